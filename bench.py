@@ -1,0 +1,320 @@
+#!/usr/bin/env python
+"""bench.py -- FastMoE MoE-layer forward+backward tokens/s on B200.
+
+Workload (BASELINE.json configs[1]) at N=1: one MoE layer,
+d_model=1024, d_hidden=4096, 64 experts, top-2, 65536 tokens, bf16 storage /
+fp32 accumulation, synthetic inputs, weights from the reference's init_state
+generators.  A step = forward + backward of the layer (gate, plan, scatter,
+grouped expert GEMMs, gather-combine, and every gradient).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Timing: W warm-up steps, then exactly K steps bracketed by barrier +
+synchronize, timed with CUDA events on the layer's stream, max over ranks.
+The working set (inputs + activations + weights ~ 7 GB) is far above the
+126 MB L2, so no flush is needed between steps.  Per-stage CUDA events are
+recorded inside the same timed region (fmoe_ctx_profile) and give the
+roofline of the dominant kernel (the tcgen05 grouped GEMM).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE-layer fwd+bwd tokens/s at 1/2/4/8 B200; expert-GEMM % of tensor peak"
+UNIT = "tokens/s"
+CFG2 = dict(n_b=65536, d_m=1024, d_h=4096, n_e_local=64, k=2)          # 1 GPU
+CFG3 = dict(n_b=16384, d_m=2048, d_h=8192, n_e_local=8, k=2)           # EP, per GPU
+SEED = 42
+STAGES = ["-", "gate", "plan", "scatter", "fc1", "fc2", "gather_combine", "fwd_bwd_gap",
+          "gather_combine_bwd", "dgrad_fc2", "wgrad_fc2", "db2", "dgrad_fc1", "wgrad_fc1", "db1",
+          "gate_dwg", "gate_dx_scatter_bwd"]
+GEMM_STAGES = ["fc1", "fc2", "dgrad_fc2", "wgrad_fc2", "dgrad_fc1", "wgrad_fc1"]
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return dict(hbm=j["hbm_gbs"], tc=j["bf16_tflops"], tc_sus=j.get("bf16_tflops_sustained", j["bf16_tflops"]),
+                    src="measured (MEASURED_PEAKS.json)")
+    return dict(hbm=6650.0, tc=1590.0, tc_sus=1400.0, src="fallback (B200_PROFILING.md)")
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, device: int):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={device}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            out = self.p.communicate(timeout=5)[0]
+        except Exception:
+            self.p.kill()
+            out = ""
+        sm, mx, reasons = [], [], set()
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------- CPU reference
+def cpu_reference(n_tokens: int, cfg: dict, min_seconds: float = 10.0, max_reps: int = 5):
+    """The reference's own forward+backward (oracle/_ref, compiled from its
+    sources) on the host cores: tokens/s on a bounded token sample of cfg."""
+    cores = os.cpu_count() or 1
+    os.environ["FMOE_THREADS"] = str(cores)
+    from oracle import bindings
+
+    if not bindings.ref_available():
+        return None
+    lib = C.CDLL(bindings.REF_SO)
+    lib.ref_bench_create.restype = C.c_void_p
+    lib.ref_bench_create.argtypes = [C.c_uint64] + [C.c_int64] * 5
+    lib.ref_bench_step.argtypes = [C.c_void_p]
+    lib.ref_bench_destroy.argtypes = [C.c_void_p]
+    h = lib.ref_bench_create(SEED, n_tokens, cfg["d_m"], cfg["d_h"], cfg["n_e_local"], cfg["k"])
+    if not h:
+        return None
+    try:
+        lib.ref_bench_step(h)  # warm-up
+        times = []
+        t_all = time.perf_counter()
+        while len(times) < max_reps and (len(times) < 2 or time.perf_counter() - t_all < min_seconds):
+            t0 = time.perf_counter()
+            lib.ref_bench_step(h)
+            times.append(time.perf_counter() - t0)
+    finally:
+        lib.ref_bench_destroy(h)
+    mean = statistics.mean(times)
+    return {"value": n_tokens / mean, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": (f"{n_tokens} tokens of d_m={cfg['d_m']} d_h={cfg['d_h']} E={cfg['n_e_local']} "
+                       f"k={cfg['k']} (the GPU workload's layer, token-subsampled), fp64, reference "
+                       f"forward+backward, warm-up 1 + {len(times)} reps, mean {mean:.2f} s/step, "
+                       f"FMOE_THREADS={cores}")}
+
+
+def cpu_tokens_for(cores: int) -> int:
+    return max(256, min(4096, 64 * cores))
+
+
+# --------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0)
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    cfg = CFG2 if world == 1 else CFG3
+    if args.impl == "reference":
+        return run_reference(args, world, rank, cfg)
+    return run_ours(args, world, rank, cfg)
+
+
+def run_reference(args, world, rank, cfg):
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    res = cpu_reference(cpu_tokens_for(cores), cfg, min_seconds=max(10.0, 2.0 * args.steps),
+                        max_reps=max(2, min(args.steps, 10)))
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libfmoe_ref.so not built"}))
+        return 0
+    line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "ms_per_step": 1e3 * cpu_tokens_for(cores) / res["value"], "dtype": "f64", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None,
+            "config": {"workload": workload_name(cfg, world), **cfg, "world": world},
+            "cpu_baseline": res,
+            "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def workload_name(cfg, world):
+    if world == 1:
+        return ("cfg2: single MoE layer d_model=1024 d_hidden=4096, 64 experts top-2, 65536 tokens, "
+                "bf16 storage / fp32 accumulate, fwd+bwd")
+    return (f"cfg3: expert-parallel MoE layer d_model=2048 d_hidden=8192, 8 experts/GPU x {world} GPUs, "
+            "top-2, 16384 tokens/GPU, fwd+bwd")
+
+
+def run_ours(args, world, rank, cfg):
+    import torch
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2103_13262_b200 as fm
+    from paper_2103_13262_b200 import _lib
+
+    n, d, h, el, k = cfg["n_b"], cfg["d_m"], cfg["d_h"], cfg["n_e_local"], cfg["k"]
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        layer = fm.MoELayer(fm.MoEConfig(n, d, h, k, el, world, SEED), rank=rank, dtype=torch.bfloat16)
+        if world > 1:
+            layer.connect(dist)
+        g = torch.Generator(device="cuda")
+        g.manual_seed(1000 + rank)
+        x = (torch.rand(n, d, device="cuda", generator=g) * 2 - 1).bfloat16()
+        dy = (torch.rand(n, d, device="cuda", generator=g) * 2 - 1).bfloat16()
+        y = torch.empty_like(x)
+        dx = torch.empty_like(x)
+
+        def step():
+            layer.forward(x, y)
+            layer.backward(dy, dx)
+
+        for _ in range(max(args.warmup, 3) if args.warmup >= 0 else 3):
+            step()
+        ctx = layer.ctx
+        _lib.check(_lib.lib.fmoe_ctx_profile(ctx.h, args.steps))
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        clocks = Clocks(local)
+        launches0 = ctx.launches
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for _ in range(args.steps):
+            step()
+        t1.record(stream)
+        torch.cuda.synchronize()
+        clk = clocks.stop()
+        if dist:
+            dist.barrier()
+        launches = ctx.launches - launches0
+        ms = t0.elapsed_time(t1) / args.steps
+        stage = (C.c_float * len(STAGES))()
+        done = C.c_int()
+        _lib.check(_lib.lib.fmoe_ctx_profile_read(ctx.h, stage, len(STAGES), C.byref(done)))
+        _lib.check(_lib.lib.fmoe_ctx_profile(ctx.h, 0))
+        stage_ms = {STAGES[i]: stage[i] / max(done.value, 1) for i in range(1, len(STAGES))}
+        if dist:
+            t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        tokens = n * world
+        value = tokens / (ms / 1e3)
+
+        # ---- end to end through the public host-buffer entry point
+        e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
+        hx = x.cpu().pin_memory()
+        hdy = dy.cpu().pin_memory()
+        hy = torch.empty_like(hx).pin_memory()
+        hdx = torch.empty_like(hx).pin_memory()
+        layer.step_host(hx, hdy, hy, hdx)
+        if dist:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            layer.step_host(hx, hdy, hy, hdx)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / e2e_steps
+        if dist:
+            t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+
+    pk = peaks()
+    flop_gemm = 2.0 * n * k * d * h  # one expert GEMM launch (fmoe_bench.cpp:110-126)
+    gemm_ms = [stage_ms[s] for s in GEMM_STAGES]
+    avg_launch_ms = sum(gemm_ms) / len(gemm_ms)
+    achieved = flop_gemm / (avg_launch_ms / 1e3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("tc_gemm_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    s = 2  # bf16
+    scatter_bytes = s * d * (n + n * k) + 4 * n * k
+    gather_bytes = s * d * (n * k + n) + 8 * n * k
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform[-1,1) inputs; reference init_state weights)",
+        "config": {"workload": workload_name(cfg, world), "n_b_per_gpu": n, "d_m": d, "d_h": h,
+                   "experts_per_gpu": el, "experts_total": el * world, "k": k,
+                   "parallelism": f"ep{world}" if world > 1 else "single",
+                   "l2": "working set ~7 GB >> 126 MB L2; no flush needed"},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "e2e": {"value": tokens / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 2 * n * d * 2,
+                "d2h_bytes_per_step": 2 * n * d * 2,
+                "path": "fmoe_layer_step_host (pinned host x,dy -> H2D -> fwd+bwd -> D2H y,dx)"},
+        "roofline": {"kernel": "tc_gemm_kernel (grouped tcgen05 expert GEMM; fc1, fc2, 2x dgrad, 2x wgrad)",
+                     "bound": "tensor", "achieved": achieved, "peak": pk["tc_sus"], "unit": "TFLOP/s",
+                     "frac": achieved / pk["tc_sus"], "frac_of_burst_peak": achieved / pk["tc"],
+                     "frac_of_datasheet_2250": achieved / 2250.0,
+                     "flops_per_launch": flop_gemm, "avg_launch_ms": avg_launch_ms, "traffic": traffic,
+                     "peak_source": pk["src"] + " bf16 sustained (kernel timed inside a long step)"},
+        "stages_ms": {k_: round(v, 4) for k_, v in stage_ms.items()},
+        "permute_roofline": {
+            "scatter_GBps": scatter_bytes / (stage_ms["scatter"] / 1e3) / 1e9,
+            "gather_combine_GBps": gather_bytes / (stage_ms["gather_combine"] / 1e3) / 1e9,
+            "peak_GBps": pk["hbm"],
+        },
+    }
+    line["permute_roofline"]["scatter_frac"] = line["permute_roofline"]["scatter_GBps"] / pk["hbm"]
+    line["permute_roofline"]["gather_frac"] = line["permute_roofline"]["gather_combine_GBps"] / pk["hbm"]
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        line["cpu_baseline"] = cpu_reference(cpu_tokens_for(cores), cfg)
+    if rank == 0:
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

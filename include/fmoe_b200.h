@@ -1,0 +1,211 @@
+/*
+ * fmoe_b200.h -- C-ABI of the B200-native FastMoE MoE-layer hot path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no torch or C++
+ * types.  Every entry point replaces one operator of the reference's C++ API
+ * (/root/reference/proj/include/fmoe/*.hpp) and is cited below.  The C++
+ * drop-in headers (include/fmoe/*.hpp, libfmoe_dropin.so) and the Python
+ * package (paper_2103_13262_b200) are thin hosts over these symbols.
+ *
+ * Conventions
+ *   - Tensor pointers are DEVICE pointers unless the name ends in _host.
+ *     Row-major, a row is one sample (matrix.hpp:12-14).
+ *   - All work is stream-ordered on the context's stream; no entry point
+ *     synchronises the host except where stated (validation, EP count
+ *     exchange, *_host copies).
+ *   - Indices are int32 on device (the reference uses int64; hosts widen).
+ *   - Status: 0 ok, else one of FMOE_ERR_*, mapping 1:1 onto the reference's
+ *     exception types (errors.hpp:8-23); fmoe_last_error() (thread-local)
+ *     holds the message.  Calls never abort the process.
+ *   - dtype selects the arithmetic: FMOE_F64 is the parity mode that
+ *     reproduces the reference's fp64 accumulation order (bit-identical on
+ *     every operator except softmax's exp); FMOE_F32 is SIMT fp32;
+ *     FMOE_BF16 is the product path: bf16 storage, fp32 accumulation on the
+ *     tcgen05 tensor cores, fp32 gate scores and fp32 weight gradients.
+ */
+#ifndef FMOE_B200_H_
+#define FMOE_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FMOE_OK 0
+#define FMOE_ERR_SHAPE 1     /* fmoe::ShapeError     (errors.hpp:8-11)  */
+#define FMOE_ERR_PROTOCOL 2  /* fmoe::ProtocolError  (errors.hpp:13-17) */
+#define FMOE_ERR_TRANSPORT 3 /* fmoe::TransportError (errors.hpp:19-23) */
+#define FMOE_ERR_CUDA 4      /* CUDA / driver failure (no reference analogue) */
+
+typedef enum { FMOE_F64 = 0, FMOE_F32 = 1, FMOE_BF16 = 2 } fmoe_dtype;
+
+const char* fmoe_last_error(void);
+const char* fmoe_version(void);
+
+/* ------------------------------------------------------------------ context */
+/* A context binds a device, a stream and a launch counter.  stream may be
+ * NULL (legacy default stream) or a cudaStream_t. */
+typedef struct fmoe_ctx fmoe_ctx;
+int fmoe_ctx_create(int device, void* stream, fmoe_ctx** out);
+int fmoe_ctx_destroy(fmoe_ctx* ctx);
+int fmoe_ctx_set_stream(fmoe_ctx* ctx, void* stream);
+/* Number of kernels this library launched through ctx (for bench accounting). */
+int64_t fmoe_ctx_launches(const fmoe_ctx* ctx);
+/* Per-stage timing of MoE-layer steps: arm n_steps x N stage events (CUDA
+ * events on the context stream, recorded by fmoe_layer_fwd/bwd; n_steps = 0
+ * disarms).  profile_read synchronises and returns, per stage, the summed
+ * milliseconds between the previous mark and this one over the recorded
+ * steps.  Stage order: 0 -, 1 gate, 2 plan, 3 scatter, 4 fc1, 5 fc2,
+ * 6 gather_combine, 7 (fwd->bwd gap), 8 gather_combine_bwd, 9 dgrad fc2,
+ * 10 wgrad fc2, 11 db2, 12 dgrad fc1, 13 wgrad fc1, 14 db1, 15 gate d_wg,
+ * 16 gate d_x + scatter_backward. */
+int fmoe_ctx_profile(fmoe_ctx* ctx, int n_steps);
+int fmoe_ctx_profile_read(fmoe_ctx* ctx, float* stage_ms, int n_stages, int* steps_done);
+/* Synchronise the stream and surface any deferred device-side error (e.g. an
+ * out-of-range expert index seen by fmoe_plan_build). */
+int fmoe_ctx_check(fmoe_ctx* ctx);
+
+/* --------------------------------------------------------------- gate (L1) */
+/* gate_forward (gate.hpp:23-27; gate.cpp:23-35): scores = softmax(x * w_g)
+ * rowwise, then the k largest scores, descending, ties -> lower expert index
+ * (matrix.cpp:172-189).  Selected scores are not renormalised.
+ *   x [n_b, d_m] dtype, w_g [d_m, E] dtype
+ *   scores [n_b, E] and topk_scores [n_b, k]: f64 when dtype == FMOE_F64, else f32
+ *   topk_idx [n_b, k] int32
+ * ShapeError when k is not in [1, E]. */
+int fmoe_gate_fwd(fmoe_ctx* ctx, fmoe_dtype dtype, const void* x, const void* w_g, int64_t n_b,
+                  int64_t d_m, int64_t n_experts, int64_t k, void* scores, int32_t* topk_idx,
+                  void* topk_scores);
+
+/* gate_backward (gate.hpp:34-38; gate.cpp:37-65): full softmax Jacobian on
+ * the selected scores.  d_topk [n_b, k] (score type), d_wg [d_m, E] (score
+ * type, overwritten), d_x [n_b, d_m] dtype (overwritten; may be NULL). */
+int fmoe_gate_bwd(fmoe_ctx* ctx, fmoe_dtype dtype, const void* x, const void* w_g,
+                  const void* scores, const int32_t* topk_idx, const void* d_topk, int64_t n_b,
+                  int64_t d_m, int64_t n_experts, int64_t k, void* d_wg, void* d_x);
+
+/* -------------------------------------------------------- dispatch plan (L1) */
+/* DispatchPlan (dispatch.hpp:15-24) on device.  Expert e owns the row block
+ * [offsets[e], offsets[e] + counts[e]) of the expanded buffers; with
+ * align == 1 offsets are exactly the reference's exclusive prefix sums and
+ * capacity == n_b*k.  With align == 128 every block starts on a 128-row
+ * tensor-core tile (rows between a block's end and the next start are padding:
+ * src_row = -1, zero-filled by fmoe_scatter / fmoe_gather_combine_bwd).
+ * Inside a block positions are ordered by (row, slot) ascending, exactly as
+ * build_plan's row-major walk (dispatch.cpp:37-45). */
+typedef struct {
+  int64_t n_b, k, n_experts, align, capacity;
+  int32_t* counts;      /* [E]                                              */
+  int32_t* offsets;     /* [E+1]  offsets[E] = padded total rows            */
+  int32_t* src_row;     /* [capacity] expanded_src_row, -1 for padding      */
+  int32_t* slot;        /* [capacity] expanded_slot                         */
+  int32_t* inverse_pos; /* [n_b*k]                                          */
+  int32_t* tile_expert; /* [capacity/128] (align==128) expert of each tile  */
+  int32_t* n_tiles;     /* [1] number of valid 128-row tiles                */
+  void* scratch;        /* fmoe_plan_sizes() scratch_bytes                  */
+} fmoe_plan;
+
+/* Sizes for a plan: capacity rows and device scratch bytes. */
+int fmoe_plan_sizes(int64_t n_b, int64_t k, int64_t n_experts, int64_t align, int64_t* capacity,
+                    int64_t* scratch_bytes);
+/* build_plan (dispatch.hpp:28; dispatch.cpp:10-47): histogram, exclusive scan
+ * and stable (row, slot) ranking on device.  Out-of-range indices are a
+ * ShapeError: reported immediately when validate != 0 (one host sync),
+ * otherwise by the next fmoe_ctx_check(). */
+int fmoe_plan_build(fmoe_ctx* ctx, const int32_t* topk_idx, fmoe_plan* plan, int validate);
+
+/* ------------------------------------------------------------ permutes (L1) */
+/* scatter (dispatch.cpp:49-59): xs[p] = x[src_row[p]]; padding rows := 0. */
+int fmoe_scatter(fmoe_ctx* ctx, fmoe_dtype dtype, const void* x, int64_t d,
+                 const fmoe_plan* plan, void* xs);
+/* gather_combine (dispatch.cpp:61-78): y[i] = sum_j w[i,j] * ys[inverse_pos[i,j]],
+ * slot order; w in score type. */
+int fmoe_gather_combine(fmoe_ctx* ctx, fmoe_dtype dtype, const void* ys, int64_t d,
+                        const fmoe_plan* plan, const void* topk_scores, void* y);
+/* scatter_backward (dispatch.cpp:80-95): d_x[i] = sum_j d_xs[inverse_pos[i,j]]. */
+int fmoe_scatter_bwd(fmoe_ctx* ctx, fmoe_dtype dtype, const void* d_xs, int64_t d,
+                     const fmoe_plan* plan, void* d_x);
+/* gather_combine_backward (dispatch.cpp:97-126): d_ys[pos] = w * d_y[i];
+ * d_topk[i,j] = <d_y[i], ys[pos]>.  Padding rows of d_ys := 0. */
+int fmoe_gather_combine_bwd(fmoe_ctx* ctx, fmoe_dtype dtype, const void* d_y, const void* ys,
+                            int64_t d, const fmoe_plan* plan, const void* topk_scores,
+                            void* d_ys, void* d_topk);
+
+/* ------------------------------------------------------------- experts (L1) */
+/* Expert pool parameters, all experts stacked: w1 [E, d_m, d_h], b1 [E, d_h],
+ * w2 [E, d_h, d_m], b2 [E, d_m] (expert.hpp:15-21).  Biases are f32 when
+ * dtype == FMOE_BF16, else dtype. */
+typedef struct {
+  const void* w1;
+  const void* b1;
+  const void* w2;
+  const void* b2;
+} fmoe_expert_params;
+/* Gradients: f32 when dtype == FMOE_BF16, else dtype. */
+typedef struct {
+  void* d_w1;
+  void* d_b1;
+  void* d_w2;
+  void* d_b2;
+} fmoe_expert_grads;
+
+/* multi_expert_forward (expert.hpp:47-53; expert.cpp:85-102): every block of
+ * `blocks` (counts/offsets of a plan, or of an EP receive layout) runs
+ * expert_forward: hidden = relu(xs*w1 + b1) (cached for backward), ys =
+ * hidden*w2 + b2.  Empty blocks are legal.  FMOE_BF16 requires d_m and d_h to
+ * be multiples of 64 and blocks->align == 128. */
+int fmoe_experts_fwd(fmoe_ctx* ctx, fmoe_dtype dtype, const fmoe_plan* blocks, int64_t d_m,
+                     int64_t d_h, fmoe_expert_params params, const void* xs, void* hidden,
+                     void* ys);
+/* multi_expert_backward (expert.hpp:60-64; expert.cpp:104-125): d_xs and all
+ * four gradients (overwritten; empty experts get zero gradients). */
+int fmoe_experts_bwd(fmoe_ctx* ctx, fmoe_dtype dtype, const fmoe_plan* blocks, int64_t d_m,
+                     int64_t d_h, fmoe_expert_params params, const void* xs, const void* hidden,
+                     const void* d_ys, void* d_xs, fmoe_expert_grads grads);
+
+/* --------------------------------------------------------- MoE layer (L3) */
+/* One rank's slice of the layer (moe_layer.hpp:17-38): config, replicated
+ * gate, local experts g = rank*n_e_local + slot, device weights, gradients and
+ * all activations/workspace sized for n_b tokens. */
+typedef struct {
+  int64_t n_b, d_m, d_h, k, n_e_local, world_size, rank;
+  uint64_t seed;
+  fmoe_dtype dtype;
+} fmoe_layer_config;
+typedef struct fmoe_layer fmoe_layer;
+
+int fmoe_layer_create(fmoe_ctx* ctx, const fmoe_layer_config* cfg, fmoe_layer** out);
+int fmoe_layer_destroy(fmoe_layer* layer);
+/* init_state (moe_layer.cpp:28-45): the reference's generators (mt19937_64,
+ * stream_seed), bit-identical fp64 values rounded once to the layer dtype. */
+int fmoe_layer_init_weights(fmoe_layer* layer);
+/* Device pointers of the parameters (w_g, w1, b1, w2, b2) and gradients
+ * (d_wg, d_w1, d_b1, d_w2, d_b2) so hosts can read/write them in place. */
+int fmoe_layer_params(fmoe_layer* layer, void** w_g, fmoe_expert_params* experts);
+int fmoe_layer_grads(fmoe_layer* layer, void** d_wg, fmoe_expert_grads* experts);
+/* Activations kept for backward (MoEForwardCache, moe_layer.hpp:42-50). */
+int fmoe_layer_routing(fmoe_layer* layer, const int32_t** topk_idx, const void** topk_scores,
+                       const void** scores, fmoe_plan* plan);
+
+/* forward (moe_layer.cpp:67-110): x [n_b, d_m] -> y [n_b, d_m], dtype. */
+int fmoe_layer_fwd(fmoe_layer* layer, const void* x, void* y);
+/* backward (moe_layer.cpp:112-142): dy -> dx and parameter gradients. */
+int fmoe_layer_bwd(fmoe_layer* layer, const void* dy, void* dx);
+/* Host-buffer step for end-to-end use: H2D x (and dy), forward, backward,
+ * D2H y (and dx).  Buffers are host memory (pinned for full speed); dy/dx may
+ * be NULL for forward only.  Synchronises before returning. */
+int fmoe_layer_step_host(fmoe_layer* layer, const void* x_host, const void* dy_host,
+                         void* y_host, void* dx_host);
+
+/* --------------------------------------------- expert parallelism (L2, EP) */
+/* Communicator over NCCL (NVLink/NVSwitch).  Rank 0 creates an id, the host
+ * broadcasts it out of band (torch.distributed store, MPI, ...). */
+int fmoe_comm_unique_id(void* id_out, int64_t id_bytes);
+int fmoe_comm_init(fmoe_ctx* ctx, const void* id, int64_t id_bytes, int world, int rank);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FMOE_B200_H_ */

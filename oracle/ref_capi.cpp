@@ -336,6 +336,50 @@ int ref_moe_distributed(const double* x, const double* dy, int64_t world, int64_
   });
 }
 
+// CPU-baseline handle: the reference's own init_state + forward/backward at a
+// given configuration, inputs from the bench generators (x stream 102, dy
+// stream 103; fmoe_bench.cpp:128-134,226-227).  Threads: FMOE_THREADS.
+struct RefBench {
+  MoELayerState st;
+  Matrix x, dy;
+};
+
+void* ref_bench_create(uint64_t seed, int64_t n, int64_t d, int64_t h, int64_t e, int64_t k) {
+  try {
+    MoEConfig cfg;
+    cfg.n_b = static_cast<std::size_t>(n);
+    cfg.d_m = static_cast<std::size_t>(d);
+    cfg.d_h = static_cast<std::size_t>(h);
+    cfg.k = static_cast<std::size_t>(k);
+    cfg.n_e_local = static_cast<std::size_t>(e);
+    cfg.world_size = 1;
+    cfg.seed = seed;
+    auto* b = new RefBench;
+    b->st = init_state(cfg, 0);
+    b->x = Matrix(static_cast<std::size_t>(n), static_cast<std::size_t>(d));
+    b->dy = Matrix(static_cast<std::size_t>(n), static_cast<std::size_t>(d));
+    UniformRng(stream_seed(seed, 102)).fill(b->x, -1.0, 1.0);
+    UniformRng(stream_seed(seed, 103)).fill(b->dy, -1.0, 1.0);
+    return b;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return nullptr;
+  }
+}
+
+int ref_bench_step(void* handle) {
+  return guarded([&] {
+    auto* b = static_cast<RefBench*>(handle);
+    MoEForwardCache cache;
+    const Matrix y = forward(b->x, b->st, nullptr, &cache);
+    auto res = backward(b->dy, cache, b->st, nullptr);
+    (void)y;
+    (void)res;
+  });
+}
+
+void ref_bench_destroy(void* handle) { delete static_cast<RefBench*>(handle); }
+
 // exchange_counts over an InProcWorld: local_counts [world][E_total] in,
 // recv_counts [world][world*e_local] out (collectives.cpp:69-109).
 int ref_exchange_counts(const int64_t* local_counts, int64_t world, int64_t total,

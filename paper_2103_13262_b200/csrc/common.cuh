@@ -1,0 +1,118 @@
+// common.cuh -- shared internals of libfmoe_b200.so (not part of the C-ABI).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "fmoe_b200.h"
+
+namespace fmoe_b200 {
+
+// ----------------------------------------------------------------- errors
+// Internal exceptions carry the C-ABI status; every extern "C" entry point
+// converts them (capi.cu), so nothing escapes the boundary.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void shape_error(const std::string& m) { throw Error(FMOE_ERR_SHAPE, m); }
+[[noreturn]] inline void protocol_error(const std::string& m) { throw Error(FMOE_ERR_PROTOCOL, m); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess)
+    throw Error(FMOE_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e) + " at " + file +
+                                   ":" + std::to_string(line));
+}
+#define CK(x) ::fmoe_b200::cuda_check((x), #x, __FILE__, __LINE__)
+#define CK_LAUNCH(ctx) \
+  do {                 \
+    (ctx)->launches++; \
+    CK(cudaGetLastError()); \
+  } while (0)
+
+// ---------------------------------------------------------------- context
+// Stage marks of one MoE-layer step (CUDA events on the layer's stream,
+// recorded only while profiling is armed; read back after the timed region).
+enum Mark : int {
+  MARK_FWD_BEGIN = 0, MARK_GATE, MARK_PLAN, MARK_SCATTER, MARK_FC1, MARK_FC2, MARK_GATHER,
+  MARK_BWD_BEGIN, MARK_GCB, MARK_DGRAD2, MARK_WGRAD2, MARK_DB2, MARK_DGRAD1, MARK_WGRAD1, MARK_DB1,
+  MARK_GATE_DWG, MARK_GATE_DX, N_MARKS
+};
+struct Prof {
+  std::vector<cudaEvent_t> ev;  // [steps][N_MARKS]
+  int steps = 0, step = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  int64_t launches = 0;
+  int* d_error = nullptr;  // deferred device-side error flag (plan validation)
+  void* comm = nullptr;    // ncclComm_t when EP is initialised
+  void* ws = nullptr;      // grow-only scratch for operator-level calls
+  size_t ws_size = 0;
+  int world = 1, rank = 0;
+  Prof* prof = nullptr;
+};
+
+inline void ctx_mark(Ctx* c, int id) {
+  Prof* p = c->prof;
+  if (!p || p->step >= p->steps) return;
+  cudaEventRecord(p->ev[(size_t)p->step * N_MARKS + id], c->stream);
+  if (id == MARK_GATE_DX) p->step++;
+}
+
+// ------------------------------------------------------------- type traits
+template <typename T>
+struct ScoreOf {
+  using type = float;
+};
+template <>
+struct ScoreOf<double> {
+  using type = double;
+};
+
+__device__ __forceinline__ float to_f(float v) { return v; }
+__device__ __forceinline__ double to_f(double v) { return v; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+template <typename T>
+__device__ __forceinline__ T from_d(double v);
+template <>
+__device__ __forceinline__ double from_d<double>(double v) { return v; }
+
+inline size_t dtype_size(fmoe_dtype t) { return t == FMOE_F64 ? 8 : t == FMOE_F32 ? 4 : 2; }
+inline size_t score_size(fmoe_dtype t) { return t == FMOE_F64 ? 8 : 4; }
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+int guard_status(const std::exception& e);
+extern thread_local std::string g_last_error;
+
+// Dispatch a templated functor on the runtime dtype.
+template <typename F>
+void dispatch_dtype(fmoe_dtype t, F&& f) {
+  switch (t) {
+    case FMOE_F64: f((double*)nullptr); break;
+    case FMOE_F32: f((float*)nullptr); break;
+    case FMOE_BF16: f((__nv_bfloat16*)nullptr); break;
+    default: shape_error("unknown dtype");
+  }
+}
+
+}  // namespace fmoe_b200

@@ -1,0 +1,204 @@
+// layer.cu -- the MoE layer (moe_layer.cpp:67-142) orchestrated on one
+// stream: gate -> plan -> scatter -> experts -> gather_combine, and the
+// backward pass in the reference's order.  All buffers are allocated once at
+// creation (sized for n_b tokens, worst-case padded expert blocks), so a
+// forward+backward step performs no allocation and no host synchronisation
+// on a single GPU.
+//
+// FMOE_BF16 (product path), per step:
+//   fwd: gate GEMM+softmax+top-k (tcgen05) | plan x3 | scatter | fc1 (tcgen05,
+//        bias+relu) | fc2 (tcgen05, bias) | gather_combine
+//   bwd: gather_combine_bwd + gate Jacobian | dgrad fc2 (relu mask) | wgrad fc2 |
+//        db2 | dgrad fc1 | wgrad fc1 | db1 | gate dWg (split-K) + reduce |
+//        gate dx fused with scatter_backward
+#include <cstring>
+#include <vector>
+
+#include "init.h"
+#include "layer.cuh"
+#include "ops.cuh"
+
+namespace fmoe_b200 {
+
+namespace {
+template <typename T>
+T* dalloc(std::vector<void*>& owned, int64_t n) {
+  void* p = nullptr;
+  const size_t bytes = std::max<int64_t>(n, 1) * sizeof(T);
+  CK(cudaMalloc(&p, bytes));
+  owned.push_back(p);
+  return reinterpret_cast<T*>(p);
+}
+void* dalloc_bytes(std::vector<void*>& owned, int64_t bytes) {
+  void* p = nullptr;
+  CK(cudaMalloc(&p, std::max<int64_t>(bytes, 256)));
+  owned.push_back(p);
+  return p;
+}
+}  // namespace
+
+Layer::Layer(Ctx* c, const fmoe_layer_config& cf) : ctx(c), cfg(cf) {
+  if (cfg.n_b < 0 || cfg.d_m < 1 || cfg.d_h < 1 || cfg.n_e_local < 1 || cfg.world_size < 1)
+    shape_error("MoEConfig: all dimensions must be at least 1");
+  E = cfg.n_e_local * cfg.world_size;
+  if (cfg.k < 1 || cfg.k > E) shape_error("MoEConfig: k must lie in [1, total experts]");
+  if (cfg.rank < 0 || cfg.rank >= cfg.world_size) shape_error("init_state: rank out of range");
+  t = cfg.dtype;
+  const bool bf = t == FMOE_BF16;
+  if (bf) {
+    if (cfg.d_m % 64 || cfg.d_h % 64)
+      shape_error("bf16 layer needs d_m and d_h to be multiples of 64");
+    if (E % 8) shape_error("bf16 layer needs a total expert count that is a multiple of 8");
+    if (cfg.k > 8) shape_error("bf16 layer supports k <= 8");
+  }
+  es = dtype_size(t);
+  ss = score_size(t);
+  gs = bf ? 4 : es;  // gradient element size
+  const int64_t n = cfg.n_b, d = cfg.d_m, h = cfg.d_h, k = cfg.k, el = cfg.n_e_local;
+  // parameters
+  wg = dalloc_bytes(owned, d * E * es);
+  w1 = dalloc_bytes(owned, el * d * h * es);
+  w2 = dalloc_bytes(owned, el * h * d * es);
+  b1 = dalloc_bytes(owned, el * h * (bf ? 4 : es));
+  b2 = dalloc_bytes(owned, el * d * (bf ? 4 : es));
+  // gradients
+  dwg = dalloc_bytes(owned, d * E * ss);
+  dw1 = dalloc_bytes(owned, el * d * h * gs);
+  dw2 = dalloc_bytes(owned, el * h * d * gs);
+  db1 = dalloc_bytes(owned, el * h * gs);
+  db2 = dalloc_bytes(owned, el * d * gs);
+  // routing
+  scores = dalloc_bytes(owned, n * E * ss);
+  vals = dalloc_bytes(owned, n * k * ss);
+  idx = dalloc<int32_t>(owned, n * k);
+  plan.n_b = n;
+  plan.k = k;
+  plan.n_experts = E;
+  plan.align = bf ? 128 : 1;
+  plan.capacity = plan_capacity(n, k, E, plan.align);
+  plan.counts = dalloc<int32_t>(owned, E);
+  plan.offsets = dalloc<int32_t>(owned, E + 1);
+  plan.src_row = dalloc<int32_t>(owned, plan.capacity);
+  plan.slot = dalloc<int32_t>(owned, plan.capacity);
+  plan.inverse_pos = dalloc<int32_t>(owned, n * k);
+  plan.tile_expert = dalloc<int32_t>(owned, plan.capacity / 128 + 1);
+  plan.n_tiles = dalloc<int32_t>(owned, 1);
+  plan.scratch = dalloc_bytes(owned, plan_scratch_bytes(n, k, E));
+  const int64_t cap = plan.capacity;
+  // activations (forward cache)
+  xs = dalloc_bytes(owned, cap * d * es);
+  hidden = dalloc_bytes(owned, cap * h * es);
+  ys = dalloc_bytes(owned, cap * d * es);
+  if (!bf || E > 256) logits = dalloc_bytes(owned, n * E * ss);
+  // backward scratch
+  d_ys = dalloc_bytes(owned, cap * d * es);
+  d_pre = dalloc_bytes(owned, cap * h * es);
+  d_xs = dalloc_bytes(owned, cap * d * es);
+  d_w = dalloc_bytes(owned, n * k * ss);
+  dz = dalloc_bytes(owned, n * E * ss);
+  dz_bf16 = dalloc<__nv_bfloat16>(owned, n * E);
+  gdx = dalloc_bytes(owned, n * d * es);
+  const int64_t S = gate_dwg_splits(n);
+  part = dalloc<float>(owned, S * d * E + S + 64);
+  if (cfg.world_size > 1) ep_alloc();
+}
+
+Layer::~Layer() {
+  for (void* p : owned) cudaFree(p);
+  if (h_stage) cudaFreeHost(h_stage);
+}
+
+fmoe_expert_params Layer::params() const { return fmoe_expert_params{w1, b1, w2, b2}; }
+fmoe_expert_grads Layer::grads() const { return fmoe_expert_grads{dw1, db1, dw2, db2}; }
+
+// init_state (moe_layer.cpp:28-45): reference generators, rounded once.
+void Layer::init_weights() {
+  const int64_t d = cfg.d_m, h = cfg.d_h, el = cfg.n_e_local;
+  std::vector<double> g(d * E), a1(el * d * h), c1(el * h), a2(el * h * d), c2(el * d);
+  init_gate_host(cfg.seed, d, E, g.data());
+  init_experts_host(cfg.seed, cfg.rank * el, el, d, h, a1.data(), c1.data(), a2.data(), c2.data());
+  auto upload = [&](const std::vector<double>& src, void* dst, fmoe_dtype as) {
+    if (as == FMOE_F64) {
+      CK(cudaMemcpy(dst, src.data(), src.size() * 8, cudaMemcpyHostToDevice));
+    } else if (as == FMOE_F32) {
+      std::vector<float> f(src.begin(), src.end());
+      CK(cudaMemcpy(dst, f.data(), f.size() * 4, cudaMemcpyHostToDevice));
+    } else {
+      std::vector<__nv_bfloat16> b(src.size());
+      for (size_t i = 0; i < src.size(); ++i) b[i] = __float2bfloat16_rn((float)src[i]);
+      CK(cudaMemcpy(dst, b.data(), b.size() * 2, cudaMemcpyHostToDevice));
+    }
+  };
+  const fmoe_dtype bias_t = t == FMOE_BF16 ? FMOE_F32 : t;
+  upload(g, wg, t);
+  upload(a1, w1, t);
+  upload(c1, b1, bias_t);
+  upload(a2, w2, t);
+  upload(c2, b2, bias_t);
+}
+
+void Layer::forward(const void* x, void* y) {
+  const int64_t n = cfg.n_b, d = cfg.d_m, h = cfg.d_h, k = cfg.k;
+  x_saved = x;
+  ctx_mark(ctx, MARK_FWD_BEGIN);
+  gate_fwd(ctx, t, x, wg, n, d, E, k, scores, idx, vals, logits);  // gate.cpp:23-35
+  ctx_mark(ctx, MARK_GATE);
+  if (cfg.world_size > 1) {
+    ep_forward(x, y);
+    fwd_done = true;
+    return;
+  }
+  plan_build(ctx, idx, plan);                                     // dispatch.cpp:10-47
+  ctx_mark(ctx, MARK_PLAN);
+  scatter(ctx, t, x, d, plan, xs);                                // dispatch.cpp:49-59
+  ctx_mark(ctx, MARK_SCATTER);
+  experts_fwd(ctx, t, plan, d, h, params(), xs, hidden, ys);      // expert.cpp:85-102
+  gather_combine(ctx, t, ys, d, plan, vals, y);                   // dispatch.cpp:61-78
+  ctx_mark(ctx, MARK_GATHER);
+  fwd_done = true;
+}
+
+void Layer::backward(const void* dy, void* dx) {
+  if (!fwd_done) protocol_error("backward: no forward cache");
+  const int64_t n = cfg.n_b, d = cfg.d_m, h = cfg.d_h, k = cfg.k;
+  if (cfg.world_size > 1) {
+    ep_backward(dy, dx);
+    return;
+  }
+  const bool bf = t == FMOE_BF16;
+  ctx_mark(ctx, MARK_BWD_BEGIN);
+  // dispatch.cpp:97-126 (+ gate.cpp:44-59 fused on the bf16 path)
+  gather_combine_bwd(ctx, t, dy, ys, d, plan, vals, d_ys, d_w, bf ? scores : nullptr, bf ? idx : nullptr,
+                     bf ? dz_bf16 : nullptr);
+  ctx_mark(ctx, MARK_GCB);
+  experts_bwd(ctx, t, plan, d, h, params(), xs, hidden, d_ys, d_xs, grads(), d_pre);  // expert.cpp:104-125
+  if (bf) {
+    gate_dwg_bf16(ctx, x_saved, dz_bf16, n, d, E, part, (float*)dwg);                  // gate.cpp:62
+    ctx_mark(ctx, MARK_GATE_DWG);
+    gate_dx_bf16(ctx, dz_bf16, wg, n, d, E, (const __nv_bfloat16*)d_xs, plan.inverse_pos, k, dx);  // gate.cpp:63 + dispatch.cpp:80-95
+  } else {
+    gate_bwd(ctx, t, x_saved, wg, scores, idx, d_w, n, d, E, k, dwg, gdx, dz, nullptr, nullptr);
+    ctx_mark(ctx, MARK_GATE_DWG);
+    scatter_bwd(ctx, t, d_xs, d, plan, dx, gdx);  // dispatch.cpp:80-95, moe_layer.cpp:140
+  }
+  ctx_mark(ctx, MARK_GATE_DX);
+}
+
+void Layer::step_host(const void* x_host, const void* dy_host, void* y_host, void* dx_host) {
+  const int64_t nd = cfg.n_b * cfg.d_m;
+  const size_t bytes = (size_t)nd * es;
+  if (!io) {
+    io = dalloc_bytes(owned, 4 * bytes);
+  }
+  uint8_t* b = reinterpret_cast<uint8_t*>(io);
+  void *x = b, *y = b + bytes, *gy = b + 2 * bytes, *gx = b + 3 * bytes;
+  CK(cudaMemcpyAsync(x, x_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  if (dy_host) CK(cudaMemcpyAsync(gy, dy_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  forward(x, y);
+  if (dy_host) backward(gy, gx);
+  CK(cudaMemcpyAsync(y_host, y, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  if (dx_host && dy_host) CK(cudaMemcpyAsync(dx_host, gx, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+}
+
+}  // namespace fmoe_b200

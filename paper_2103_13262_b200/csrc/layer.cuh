@@ -1,0 +1,52 @@
+// layer.cuh -- MoE layer state (moe_layer.hpp:17-66) on device.
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace fmoe_b200 {
+
+struct Layer {
+  Ctx* ctx;
+  fmoe_layer_config cfg;
+  int64_t E = 0;  // total experts
+  fmoe_dtype t;
+  size_t es = 0, ss = 0, gs = 0;
+  std::vector<void*> owned;
+  // parameters (gate replicated, local experts in slot order)
+  void *wg = nullptr, *w1 = nullptr, *b1 = nullptr, *w2 = nullptr, *b2 = nullptr;
+  // gradients
+  void *dwg = nullptr, *dw1 = nullptr, *db1 = nullptr, *dw2 = nullptr, *db2 = nullptr;
+  // forward cache (MoEForwardCache, moe_layer.hpp:42-50)
+  const void* x_saved = nullptr;  // caller keeps x alive until backward
+  void *scores = nullptr, *vals = nullptr, *logits = nullptr;
+  int32_t* idx = nullptr;
+  fmoe_plan plan{};
+  void *xs = nullptr, *hidden = nullptr, *ys = nullptr;
+  bool fwd_done = false;
+  // backward scratch
+  void *d_ys = nullptr, *d_pre = nullptr, *d_xs = nullptr, *d_w = nullptr, *dz = nullptr, *gdx = nullptr;
+  __nv_bfloat16* dz_bf16 = nullptr;
+  float* part = nullptr;
+  // host-buffer step
+  void* io = nullptr;
+  void* h_stage = nullptr;
+  // expert parallelism (ep.cu)
+  struct Ep;
+  Ep* ep = nullptr;
+
+  Layer(Ctx* c, const fmoe_layer_config& cf);
+  ~Layer();
+  fmoe_expert_params params() const;
+  fmoe_expert_grads grads() const;
+  void init_weights();
+  void forward(const void* x, void* y);
+  void backward(const void* dy, void* dx);
+  void step_host(const void* x_host, const void* dy_host, void* y_host, void* dx_host);
+  void ep_alloc();
+  void ep_forward(const void* x, void* y);
+  void ep_backward(const void* dy, void* dx);
+};
+
+}  // namespace fmoe_b200

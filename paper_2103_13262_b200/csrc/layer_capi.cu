@@ -1,0 +1,86 @@
+// layer_capi.cu -- extern "C" entry points of the MoE layer (fmoe_layer_*).
+#include "layer.cuh"
+
+using namespace fmoe_b200;
+
+#define FMOE_GUARD(...)               \
+  try {                               \
+    __VA_ARGS__;                      \
+    return FMOE_OK;                   \
+  } catch (const std::exception& e) { \
+    return guard_status(e);           \
+  } catch (...) {                     \
+    g_last_error = "unknown error";   \
+    return FMOE_ERR_CUDA;             \
+  }
+
+namespace {
+Layer* L(fmoe_layer* l) {
+  if (!l) shape_error("null layer");
+  return reinterpret_cast<Layer*>(l);
+}
+}  // namespace
+
+extern "C" {
+
+int fmoe_layer_create(fmoe_ctx* ctx, const fmoe_layer_config* cfg, fmoe_layer** out) {
+  FMOE_GUARD({
+    if (!ctx || !cfg || !out) shape_error("fmoe_layer_create: null argument");
+    *out = reinterpret_cast<fmoe_layer*>(new Layer(reinterpret_cast<Ctx*>(ctx), *cfg));
+  })
+}
+
+int fmoe_layer_destroy(fmoe_layer* layer) { FMOE_GUARD(delete L(layer)) }
+
+int fmoe_layer_init_weights(fmoe_layer* layer) { FMOE_GUARD(L(layer)->init_weights()) }
+
+int fmoe_layer_params(fmoe_layer* layer, void** w_g, fmoe_expert_params* experts) {
+  FMOE_GUARD({
+    Layer* l = L(layer);
+    if (w_g) *w_g = l->wg;
+    if (experts) *experts = l->params();
+  })
+}
+
+int fmoe_layer_grads(fmoe_layer* layer, void** d_wg, fmoe_expert_grads* experts) {
+  FMOE_GUARD({
+    Layer* l = L(layer);
+    if (d_wg) *d_wg = l->dwg;
+    if (experts) *experts = l->grads();
+  })
+}
+
+int fmoe_layer_routing(fmoe_layer* layer, const int32_t** topk_idx, const void** topk_scores,
+                       const void** scores, fmoe_plan* plan) {
+  FMOE_GUARD({
+    Layer* l = L(layer);
+    if (topk_idx) *topk_idx = l->idx;
+    if (topk_scores) *topk_scores = l->vals;
+    if (scores) *scores = l->scores;
+    if (plan) *plan = l->plan;
+  })
+}
+
+int fmoe_layer_fwd(fmoe_layer* layer, const void* x, void* y) {
+  FMOE_GUARD({
+    if (!x || !y) shape_error("forward: null x or y");
+    L(layer)->forward(x, y);
+  })
+}
+
+int fmoe_layer_bwd(fmoe_layer* layer, const void* dy, void* dx) {
+  FMOE_GUARD({
+    if (!dy || !dx) shape_error("backward: null dy or dx");
+    L(layer)->backward(dy, dx);
+  })
+}
+
+int fmoe_layer_step_host(fmoe_layer* layer, const void* x_host, const void* dy_host, void* y_host,
+                         void* dx_host) {
+  FMOE_GUARD({
+    if (!x_host || !y_host) shape_error("step_host: null x or y");
+    L(layer)->step_host(x_host, dy_host, y_host, dx_host);
+  })
+}
+
+}  // extern "C"

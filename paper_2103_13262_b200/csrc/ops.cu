@@ -1,0 +1,325 @@
+// ops.cu -- gate and expert-pool operators for every dtype.
+//
+// FMOE_F64 / FMOE_F32 run the SIMT kernels (gemm_simt.cu, gate.cu) in the
+// reference's accumulation order.  FMOE_BF16 runs the tcgen05 grouped GEMM
+// (tc_gemm.cu): operands are used in their stored layouts through K-major or
+// MN-major TMA descriptors, so no transpose is ever materialised.
+#include <algorithm>
+#include <vector>
+
+#include "gemm_simt.cuh"
+#include "ops.cuh"
+#include "tc_gemm.cuh"
+
+namespace fmoe_b200 {
+
+void* ctx_workspace(Ctx* ctx, size_t bytes);
+
+namespace {
+
+__global__ void fill_split_offsets(int32_t* off, int64_t n_splits, int64_t rows_per_split, int64_t n) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s <= n_splits) off[s] = (int32_t)std::min<int64_t>(s * rows_per_split, n);
+}
+
+__global__ void cast_f32_bf16(const float* __restrict__ in, __nv_bfloat16* __restrict__ out, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __float2bfloat16_rn(in[i]);
+}
+
+int pick_bn(int64_t n) { return n <= 64 ? 64 : n <= 128 ? 128 : 256; }
+
+void require_bf16_dims(int64_t d, int64_t h) {
+  if (d % 64 || h % 64)
+    shape_error("bf16 tensor-core path needs d_m and d_h to be multiples of 64 (got " +
+                std::to_string(d) + ", " + std::to_string(h) + ")");
+}
+
+std::vector<int32_t> host_counts(Ctx* ctx, const fmoe_plan& b) {
+  std::vector<int32_t> c((size_t)b.n_experts);
+  if (!c.empty())
+    CK(cudaMemcpyAsync(c.data(), b.counts, c.size() * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return c;
+}
+
+}  // namespace
+
+int64_t gate_dwg_splits(int64_t n) {
+  // ~2 waves of (d/128 x 1) tiles over 148 SMs; each split a multiple of 64 rows
+  return std::max<int64_t>(1, std::min<int64_t>(37, ceil_div(n, 512)));
+}
+
+// ---------------------------------------------------------------- gate fwd
+void gate_fwd(Ctx* ctx, fmoe_dtype t, const void* x, const void* wg, int64_t n, int64_t d, int64_t e,
+              int64_t k, void* scores, int32_t* idx, void* vals, void* logits_ws) {
+  if (k < 1 || k > e) shape_error("gate_forward: k out of range");
+  if (n == 0) return;
+  if (t == FMOE_F64 || t == FMOE_F32) {
+    auto run = [&](auto* tag) {
+      using T = std::remove_pointer_t<decltype(tag)>;
+      SimtParams<T> p;
+      p.M = n; p.N = e; p.K = d;
+      p.A = (const T*)x; p.sa_m = d; p.sa_k = 1;
+      p.B = (const T*)wg; p.sb_k = e; p.sb_n = 1;
+      p.C = (T*)logits_ws; p.ldc = e;
+      simt_gemm<T>(ctx, p, n);
+    };
+    if (t == FMOE_F64) run((double*)nullptr); else run((float*)nullptr);
+    gate_softmax_topk(ctx, t, logits_ws, n, e, k, scores, idx, vals, false);
+    return;
+  }
+  // bf16: x [n, d] K-major; Wg [d, E] used MN-major (B(k=c, n=e) = Wg[c][e]).
+  if (d % 64) shape_error("bf16 gate needs d_m multiple of 64");
+  if (e % 8) shape_error("bf16 gate needs the expert count to be a multiple of 8");
+  const CUtensorMap ta = tc::make_tmap(x, d, n, d * 2, 64, 128);
+  const CUtensorMap tb = tc::make_tmap(wg, e, d, e * 2, 64, 64);
+  tc::Params p{};
+  p.mode = tc::RAGGED_M;
+  p.M = (int)n; p.N = (int)e; p.K = (int)d;
+  if (e <= 256) {
+    p.epi = tc::EPI_GATE;
+    p.scores = (float*)scores;
+    p.topk_idx = idx;
+    p.topk_val = (float*)vals;
+    p.topk = k <= 8 ? (int)k : 0;
+    const int bn = pick_bn(e);
+    tc::launch(ctx, bn, false, true, ta, tb, p, ceil_div(n, 128));
+    if (k > 8) gate_softmax_topk(ctx, FMOE_F32, nullptr, n, e, k, scores, idx, vals, true);
+  } else {
+    p.epi = tc::EPI_F32;
+    p.C = logits_ws; p.ldc = e;
+    tc::launch(ctx, 256, false, true, ta, tb, p, ceil_div(n, 128) * ceil_div(e, 256));
+    gate_softmax_topk(ctx, FMOE_F32, logits_ws, n, e, k, scores, idx, vals, false);
+  }
+}
+
+// ---------------------------------------------------------------- gate bwd
+void gate_dwg_bf16(Ctx* ctx, const void* x, const __nv_bfloat16* dz, int64_t n, int64_t d, int64_t e,
+                   float* part_ws, float* d_wg) {
+  const int64_t S = gate_dwg_splits(n);
+  const int64_t per = ceil_div(ceil_div(n, S), 64) * 64;
+  int32_t* offs = reinterpret_cast<int32_t*>(part_ws + S * d * e);
+  fill_split_offsets<<<1, 64, 0, ctx->stream>>>(offs, S, per, n);
+  CK_LAUNCH(ctx);
+  const CUtensorMap ta = tc::make_tmap(x, d, n, d * 2, 64, 64);   // x^T: MN-major
+  const CUtensorMap tb = tc::make_tmap(dz, e, n, e * 2, 64, 64);  // dz: MN-major
+  tc::Params p{};
+  p.mode = tc::RAGGED_K;
+  p.M = (int)d; p.N = (int)e; p.n_groups = (int)S; p.k_offsets = offs;
+  p.epi = tc::EPI_F32; p.C = part_ws; p.ldc = e; p.c_group_stride = d * e;
+  const int bn = pick_bn(e);
+  tc::launch(ctx, bn, true, true, ta, tb, p, S * ceil_div(d, 128) * ceil_div(e, bn));
+  reduce_splits(ctx, part_ws, S, d * e, d_wg);
+}
+
+void gate_dx_bf16(Ctx* ctx, const __nv_bfloat16* dz, const void* wg, int64_t n, int64_t d, int64_t e,
+                  const __nv_bfloat16* d_xs, const int32_t* inverse_pos, int64_t k, void* d_x) {
+  const CUtensorMap ta = tc::make_tmap(dz, e, n, e * 2, 64, 128);   // dz [n, E] K-major
+  const CUtensorMap tb = tc::make_tmap(wg, e, d, e * 2, 64, 256);   // Wg^T: B(k=e, n=c) = Wg[c][e], K-major
+  tc::Params p{};
+  p.mode = tc::RAGGED_M;
+  p.M = (int)n; p.N = (int)d; p.K = (int)e;
+  p.epi = d_xs ? tc::EPI_GATE_DX : tc::EPI_BF16;
+  p.C = d_x; p.ldc = d;
+  p.gather_src = d_xs; p.inverse_pos = inverse_pos; p.gk = (int)k;
+  tc::launch(ctx, 256, false, false, ta, tb, p, ceil_div(n, 128) * ceil_div(d, 256));
+}
+
+void gate_bwd(Ctx* ctx, fmoe_dtype t, const void* x, const void* wg, const void* scores,
+              const int32_t* idx, const void* d_topk, int64_t n, int64_t d, int64_t e, int64_t k,
+              void* d_wg, void* d_x, void* dz_ws, __nv_bfloat16* dz_bf16, float* part_ws) {
+  if (n == 0) {
+    const size_t bytes = (size_t)(d * e) * score_size(t);
+    if (bytes) CK(cudaMemsetAsync(d_wg, 0, bytes, ctx->stream));
+    return;
+  }
+  gate_dlogits(ctx, t, scores, idx, d_topk, n, e, k, dz_ws);
+  if (t == FMOE_F64 || t == FMOE_F32) {
+    auto run = [&](auto* tag) {
+      using T = std::remove_pointer_t<decltype(tag)>;
+      SimtParams<T> p;  // d_wg = x^T dz, sum over rows ascending (gate.cpp:62)
+      p.M = d; p.N = e; p.K = n;
+      p.A = (const T*)x; p.sa_m = 1; p.sa_k = d;
+      p.B = (const T*)dz_ws; p.sb_k = e; p.sb_n = 1;
+      p.C = (T*)d_wg; p.ldc = e;
+      simt_gemm<T>(ctx, p, d);
+      if (d_x) {  // d_x = dz Wg^T, sum over experts ascending (gate.cpp:63)
+        SimtParams<T> q;
+        q.M = n; q.N = d; q.K = e;
+        q.A = (const T*)dz_ws; q.sa_m = e; q.sa_k = 1;
+        q.B = (const T*)wg; q.sb_k = 1; q.sb_n = e;
+        q.C = (T*)d_x; q.ldc = d;
+        simt_gemm<T>(ctx, q, n);
+      }
+    };
+    if (t == FMOE_F64) run((double*)nullptr); else run((float*)nullptr);
+    return;
+  }
+  cast_f32_bf16<<<(unsigned)ceil_div(n * e, 256), 256, 0, ctx->stream>>>((const float*)dz_ws, dz_bf16, n * e);
+  CK_LAUNCH(ctx);
+  gate_dwg_bf16(ctx, x, dz_bf16, n, d, e, part_ws, (float*)d_wg);
+  if (d_x) gate_dx_bf16(ctx, dz_bf16, wg, n, d, e, nullptr, nullptr, 0, d_x);
+}
+
+// ----------------------------------------------------------------- experts
+void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
+                 const fmoe_expert_params& w, const void* xs, void* hidden, void* ys) {
+  const int64_t E = b.n_experts;
+  if (E == 0 || b.capacity == 0) return;
+  if (t == FMOE_F64 || t == FMOE_F32) {
+    const auto cnt = host_counts(ctx, b);
+    const int64_t max_m = cnt.empty() ? 0 : *std::max_element(cnt.begin(), cnt.end());
+    if (max_m == 0) return;
+    auto run = [&](auto* tag) {
+      using T = std::remove_pointer_t<decltype(tag)>;
+      SimtParams<T> p;  // hidden = relu(xs W1 + b1)   (expert.cpp:30-31)
+      p.mode = SIMT_RAGGED_M; p.G = E; p.offsets = b.offsets; p.counts = b.counts;
+      p.N = h; p.K = d;
+      p.A = (const T*)xs; p.sa_m = d; p.sa_k = 1;
+      p.B = (const T*)w.w1; p.sb_k = h; p.sb_n = 1; p.b_group_stride = d * h;
+      p.C = (T*)hidden; p.ldc = h;
+      p.bias = (const T*)w.b1; p.bias_group_stride = h; p.relu = 1;
+      simt_gemm<T>(ctx, p, max_m);
+      SimtParams<T> q;  // ys = hidden W2 + b2       (expert.cpp:32)
+      q.mode = SIMT_RAGGED_M; q.G = E; q.offsets = b.offsets; q.counts = b.counts;
+      q.N = d; q.K = h;
+      q.A = (const T*)hidden; q.sa_m = h; q.sa_k = 1;
+      q.B = (const T*)w.w2; q.sb_k = d; q.sb_n = 1; q.b_group_stride = h * d;
+      q.C = (T*)ys; q.ldc = d;
+      q.bias = (const T*)w.b2; q.bias_group_stride = d;
+      simt_gemm<T>(ctx, q, max_m);
+    };
+    if (t == FMOE_F64) run((double*)nullptr); else run((float*)nullptr);
+    return;
+  }
+  require_bf16_dims(d, h);
+  if (b.align != 128 || !b.tile_expert) shape_error("bf16 experts need a 128-aligned plan");
+  const int64_t cap = b.capacity;
+  const int64_t max_tiles = cap / 128;
+  {  // fc1: A = xs [cap, d] K-major; B = W1 [E*d, h] MN-major
+    const CUtensorMap ta = tc::make_tmap(xs, d, cap, d * 2, 64, 128);
+    const CUtensorMap tb = tc::make_tmap(w.w1, h, E * d, h * 2, 64, 64);
+    tc::Params p{};
+    p.mode = tc::RAGGED_M; p.M = (int)cap; p.N = (int)h; p.K = (int)d;
+    p.tile_group = b.tile_expert; p.n_mtiles = b.n_tiles; p.b_group_rows = (int)d;
+    p.epi = tc::EPI_BF16; p.C = hidden; p.ldc = h;
+    p.bias = (const float*)w.b1; p.bias_group_stride = h; p.relu = 1;
+    tc::launch(ctx, 256, false, true, ta, tb, p, max_tiles * ceil_div(h, 256));
+    ctx_mark(ctx, MARK_FC1);
+  }
+  {  // fc2: A = hidden [cap, h] K-major; B = W2 [E*h, d] MN-major
+    const CUtensorMap ta = tc::make_tmap(hidden, h, cap, h * 2, 64, 128);
+    const CUtensorMap tb = tc::make_tmap(w.w2, d, E * h, d * 2, 64, 64);
+    tc::Params p{};
+    p.mode = tc::RAGGED_M; p.M = (int)cap; p.N = (int)d; p.K = (int)h;
+    p.tile_group = b.tile_expert; p.n_mtiles = b.n_tiles; p.b_group_rows = (int)h;
+    p.epi = tc::EPI_BF16; p.C = ys; p.ldc = d;
+    p.bias = (const float*)w.b2; p.bias_group_stride = d; p.relu = 0;
+    tc::launch(ctx, 256, false, true, ta, tb, p, max_tiles * ceil_div(d, 256));
+    ctx_mark(ctx, MARK_FC2);
+  }
+}
+
+void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
+                 const fmoe_expert_params& w, const void* xs, const void* hidden, const void* d_ys,
+                 void* d_xs, const fmoe_expert_grads& g, void* d_pre) {
+  const int64_t E = b.n_experts;
+  if (E == 0) return;
+  if (t == FMOE_F64 || t == FMOE_F32) {
+    const auto cnt = host_counts(ctx, b);
+    const int64_t max_m = cnt.empty() ? 0 : *std::max_element(cnt.begin(), cnt.end());
+    auto run = [&](auto* tag) {
+      using T = std::remove_pointer_t<decltype(tag)>;
+      {  // d_w2 = hidden^T d_y (expert.cpp:42)
+        SimtParams<T> p;
+        p.mode = SIMT_RAGGED_K; p.G = E; p.offsets = b.offsets; p.counts = b.counts;
+        p.M = h; p.N = d;
+        p.A = (const T*)hidden; p.sa_m = 1; p.sa_k = h;
+        p.B = (const T*)d_ys; p.sb_k = d; p.sb_n = 1;
+        p.C = (T*)g.d_w2; p.ldc = d; p.c_group_stride = h * d;
+        simt_gemm<T>(ctx, p, h);
+      }
+      block_colsum(ctx, t, d_ys, d, b.offsets, b.counts, E, g.d_b2);  // expert.cpp:43-45
+      if (max_m > 0) {  // d_pre = relu_backward(d_y W2^T, preact) (expert.cpp:47-48)
+        SimtParams<T> p;
+        p.mode = SIMT_RAGGED_M; p.G = E; p.offsets = b.offsets; p.counts = b.counts;
+        p.N = h; p.K = d;
+        p.A = (const T*)d_ys; p.sa_m = d; p.sa_k = 1;
+        p.B = (const T*)w.w2; p.sb_k = 1; p.sb_n = d; p.b_group_stride = h * d;
+        p.C = (T*)d_pre; p.ldc = h;
+        p.mask = (const T*)hidden; p.ldm = h;
+        simt_gemm<T>(ctx, p, max_m);
+      }
+      {  // d_w1 = x^T d_pre (expert.cpp:50)
+        SimtParams<T> p;
+        p.mode = SIMT_RAGGED_K; p.G = E; p.offsets = b.offsets; p.counts = b.counts;
+        p.M = d; p.N = h;
+        p.A = (const T*)xs; p.sa_m = 1; p.sa_k = d;
+        p.B = (const T*)d_pre; p.sb_k = h; p.sb_n = 1;
+        p.C = (T*)g.d_w1; p.ldc = h; p.c_group_stride = d * h;
+        simt_gemm<T>(ctx, p, d);
+      }
+      block_colsum(ctx, t, d_pre, h, b.offsets, b.counts, E, g.d_b1);  // expert.cpp:51-53
+      if (max_m > 0) {  // d_x = d_pre W1^T (expert.cpp:55)
+        SimtParams<T> p;
+        p.mode = SIMT_RAGGED_M; p.G = E; p.offsets = b.offsets; p.counts = b.counts;
+        p.N = d; p.K = h;
+        p.A = (const T*)d_pre; p.sa_m = h; p.sa_k = 1;
+        p.B = (const T*)w.w1; p.sb_k = 1; p.sb_n = h; p.b_group_stride = d * h;
+        p.C = (T*)d_xs; p.ldc = d;
+        simt_gemm<T>(ctx, p, max_m);
+      }
+    };
+    if (t == FMOE_F64) run((double*)nullptr); else run((float*)nullptr);
+    return;
+  }
+  require_bf16_dims(d, h);
+  if (b.align != 128 || !b.tile_expert) shape_error("bf16 experts need a 128-aligned plan");
+  const int64_t cap = b.capacity;
+  const int64_t max_tiles = cap / 128;
+  {  // dgrad fc2: d_pre = (d_ys W2^T) * (hidden > 0); B(k=c, n=j) = W2[e][j][c] -> K-major [E*h, d]
+    const CUtensorMap ta = tc::make_tmap(d_ys, d, cap, d * 2, 64, 128);
+    const CUtensorMap tb = tc::make_tmap(w.w2, d, E * h, d * 2, 64, 256);
+    tc::Params p{};
+    p.mode = tc::RAGGED_M; p.M = (int)cap; p.N = (int)h; p.K = (int)d;
+    p.tile_group = b.tile_expert; p.n_mtiles = b.n_tiles; p.b_group_rows = (int)h;
+    p.epi = tc::EPI_MASK_BF16; p.C = d_pre; p.ldc = h; p.mask = (const __nv_bfloat16*)hidden; p.ldm = h;
+    tc::launch(ctx, 256, false, false, ta, tb, p, max_tiles * ceil_div(h, 256));
+    ctx_mark(ctx, MARK_DGRAD2);
+  }
+  {  // wgrad fc2: d_w2[e] = hidden_e^T d_ys_e  (M = h, N = d, K = rows of e)
+    const CUtensorMap ta = tc::make_tmap(hidden, h, cap, h * 2, 64, 64);
+    const CUtensorMap tb = tc::make_tmap(d_ys, d, cap, d * 2, 64, 64);
+    tc::Params p{};
+    p.mode = tc::RAGGED_K; p.M = (int)h; p.N = (int)d; p.n_groups = (int)E; p.k_offsets = b.offsets;
+    p.epi = tc::EPI_F32; p.C = g.d_w2; p.ldc = d; p.c_group_stride = h * d;
+    tc::launch(ctx, 256, true, true, ta, tb, p, E * ceil_div(h, 128) * ceil_div(d, 256));
+    ctx_mark(ctx, MARK_WGRAD2);
+  }
+  block_colsum(ctx, t, d_ys, d, b.offsets, b.counts, E, g.d_b2);
+  ctx_mark(ctx, MARK_DB2);
+  {  // dgrad fc1: d_xs = d_pre W1^T; B(k=j, n=c) = W1[e][c][j] -> K-major [E*d, h]
+    const CUtensorMap ta = tc::make_tmap(d_pre, h, cap, h * 2, 64, 128);
+    const CUtensorMap tb = tc::make_tmap(w.w1, h, E * d, h * 2, 64, 256);
+    tc::Params p{};
+    p.mode = tc::RAGGED_M; p.M = (int)cap; p.N = (int)d; p.K = (int)h;
+    p.tile_group = b.tile_expert; p.n_mtiles = b.n_tiles; p.b_group_rows = (int)d;
+    p.epi = tc::EPI_BF16; p.C = d_xs; p.ldc = d;
+    tc::launch(ctx, 256, false, false, ta, tb, p, max_tiles * ceil_div(d, 256));
+    ctx_mark(ctx, MARK_DGRAD1);
+  }
+  {  // wgrad fc1: d_w1[e] = xs_e^T d_pre_e  (M = d, N = h)
+    const CUtensorMap ta = tc::make_tmap(xs, d, cap, d * 2, 64, 64);
+    const CUtensorMap tb = tc::make_tmap(d_pre, h, cap, h * 2, 64, 64);
+    tc::Params p{};
+    p.mode = tc::RAGGED_K; p.M = (int)d; p.N = (int)h; p.n_groups = (int)E; p.k_offsets = b.offsets;
+    p.epi = tc::EPI_F32; p.C = g.d_w1; p.ldc = h; p.c_group_stride = d * h;
+    tc::launch(ctx, 256, true, true, ta, tb, p, E * ceil_div(d, 128) * ceil_div(h, 256));
+    ctx_mark(ctx, MARK_WGRAD1);
+  }
+  block_colsum(ctx, t, d_pre, h, b.offsets, b.counts, E, g.d_b1);
+  ctx_mark(ctx, MARK_DB1);
+}
+
+}  // namespace fmoe_b200

@@ -1,0 +1,35 @@
+// ops.cuh -- internal operator entry points shared by the C-ABI and the layer.
+#pragma once
+
+#include "common.cuh"
+#include "plan.cuh"
+
+namespace fmoe_b200 {
+
+// Device scratch owned by the context (grow-only; the layer preallocates so
+// its hot path never reallocates).
+void* ctx_workspace(Ctx* ctx, size_t bytes);
+
+void gate_fwd(Ctx* ctx, fmoe_dtype t, const void* x, const void* wg, int64_t n, int64_t d, int64_t e,
+              int64_t k, void* scores, int32_t* idx, void* vals, void* logits_ws);
+// dz_ws: [n, e] in score type (and a bf16 copy for FMOE_BF16 when dz_bf16 != null);
+// part_ws: fp32 split-K partials for the bf16 d_wg.
+void gate_bwd(Ctx* ctx, fmoe_dtype t, const void* x, const void* wg, const void* scores,
+              const int32_t* idx, const void* d_topk, int64_t n, int64_t d, int64_t e, int64_t k,
+              void* d_wg, void* d_x, void* dz_ws, __nv_bfloat16* dz_bf16, float* part_ws);
+// d_wg of the bf16 path from a bf16 dz (tensor cores, deterministic split-K).
+void gate_dwg_bf16(Ctx* ctx, const void* x, const __nv_bfloat16* dz, int64_t n, int64_t d, int64_t e,
+                   float* part_ws, float* d_wg);
+int64_t gate_dwg_splits(int64_t n);
+// bf16 d_x of the gate (+ scatter_backward when d_xs/inverse_pos are given).
+void gate_dx_bf16(Ctx* ctx, const __nv_bfloat16* dz, const void* wg, int64_t n, int64_t d, int64_t e,
+                  const __nv_bfloat16* d_xs, const int32_t* inverse_pos, int64_t k, void* d_x);
+
+void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
+                 const fmoe_expert_params& w, const void* xs, void* hidden, void* ys);
+// d_pre_ws: [capacity, h] dtype scratch
+void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
+                 const fmoe_expert_params& w, const void* xs, const void* hidden, const void* d_ys,
+                 void* d_xs, const fmoe_expert_grads& g, void* d_pre_ws);
+
+}  // namespace fmoe_b200

@@ -1,0 +1,382 @@
+// permute.cu -- local_scatter / local_gather (+ weighted combine) and their
+// backward passes (dispatch.cpp:49-126), HBM-bound row permutations.
+//
+// One warp per token row; rows move as 128-bit vectors with several loads in
+// flight per lane.  scatter reads each token once and writes its k copies
+// (algorithmic bytes s*d*(N + N*k)); gather_combine reads the k expert rows
+// and writes the token once.  Accumulation follows the reference's slot
+// order (fma chain for the combine, plain adds for scatter_backward) in the
+// accumulate type (fp64 for FMOE_F64, fp32 otherwise), so FMOE_F64 results
+// are bit-identical to dispatch.cpp.
+#include <type_traits>
+
+#include "common.cuh"
+#include "plan.cuh"
+
+namespace fmoe_b200 {
+
+namespace {
+
+template <typename T>
+using AccOf = typename std::conditional<std::is_same<T, double>::value, double, float>::type;
+
+template <typename T>
+struct Vec {
+  static constexpr int N = 16 / sizeof(T);
+};
+
+template <typename T, typename A>
+__device__ __forceinline__ void unpack16(const uint4& u, A (&o)[Vec<T>::N]) {
+  const T* p = reinterpret_cast<const T*>(&u);
+#pragma unroll
+  for (int i = 0; i < Vec<T>::N; ++i) o[i] = (A)to_f(p[i]);
+}
+template <typename T, typename A>
+__device__ __forceinline__ uint4 pack16(const A (&o)[Vec<T>::N]) {
+  uint4 u;
+  T* p = reinterpret_cast<T*>(&u);
+#pragma unroll
+  for (int i = 0; i < Vec<T>::N; ++i) {
+    if constexpr (std::is_same<T, double>::value)
+      p[i] = o[i];
+    else
+      p[i] = from_f<T>((float)o[i]);
+  }
+  return u;
+}
+
+__device__ __forceinline__ int64_t warp_id_global() {
+  return ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+}
+
+// Pad rows of an aligned plan: warp slot `w` -> (expert, r < 128).
+__device__ __forceinline__ int64_t pad_row(const fmoe_plan& p, int64_t w) {
+  const int e = (int)(w >> 7), r = (int)(w & 127);
+  const int64_t row = (int64_t)p.offsets[e] + p.counts[e] + r;
+  return row < p.offsets[e + 1] ? row : -1;
+}
+
+// ------------------------------------------------------------------ scatter
+// Pure byte copy: element type only sets the row size.
+__global__ void scatter_kernel(const uint8_t* __restrict__ x, int64_t row_bytes, fmoe_plan p,
+                               uint8_t* __restrict__ xs) {
+  const int64_t w = warp_id_global();
+  const int lane = threadIdx.x & 31;
+  const int k = (int)p.k;
+  if (w < p.n_b) {
+    const uint8_t* src = x + w * row_bytes;
+    int64_t dst[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dst[j] = j < k ? (int64_t)__ldg(p.inverse_pos + w * k + j) * row_bytes : 0;
+    if ((row_bytes & 15) == 0) {
+      const int64_t n16 = row_bytes >> 4;
+      const uint4* s4 = reinterpret_cast<const uint4*>(src);
+      for (int64_t c = lane; c < n16; c += 32 * 4) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (c + u * 32 < n16) v[u] = __ldg(s4 + c + u * 32);
+        for (int j = 0; j < k; ++j) {
+          uint4* d4 = reinterpret_cast<uint4*>(xs + (j < 8 ? dst[j] : (int64_t)__ldg(p.inverse_pos + w * k + j) * row_bytes));
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (c + u * 32 < n16) d4[c + u * 32] = v[u];
+        }
+      }
+    } else {
+      for (int64_t c = lane; c < row_bytes; c += 32) {
+        const uint8_t v = src[c];
+        for (int j = 0; j < k; ++j)
+          xs[(int64_t)__ldg(p.inverse_pos + w * k + j) * row_bytes + c] = v;
+      }
+    }
+    return;
+  }
+  if (p.align <= 1) return;
+  const int64_t row = pad_row(p, w - p.n_b);
+  if (row < 0) return;
+  uint8_t* d = xs + row * row_bytes;
+  if ((row_bytes & 15) == 0) {
+    uint4* d4 = reinterpret_cast<uint4*>(d);
+    for (int64_t c = lane; c < (row_bytes >> 4); c += 32) d4[c] = make_uint4(0, 0, 0, 0);
+  } else {
+    for (int64_t c = lane; c < row_bytes; c += 32) d[c] = 0;
+  }
+}
+
+// ----------------------------------------------------------- gather_combine
+template <typename T, typename S>
+__global__ void gather_combine_kernel(const T* __restrict__ ys, int64_t d, fmoe_plan p,
+                                      const S* __restrict__ w, T* __restrict__ y) {
+  using A = AccOf<T>;
+  constexpr int V = Vec<T>::N;
+  const int64_t i = warp_id_global();
+  const int lane = threadIdx.x & 31;
+  if (i >= p.n_b) return;
+  const int k = (int)p.k;
+  if ((d % V) == 0) {
+    const int64_t nv = d / V;
+    for (int64_t c = lane; c < nv; c += 32) {
+      A acc[V];
+#pragma unroll
+      for (int u = 0; u < V; ++u) acc[u] = A(0);
+      for (int j = 0; j < k; ++j) {
+        const int64_t pos = __ldg(p.inverse_pos + i * k + j);
+        const A wt = (A)__ldg(w + i * k + j);
+        A yv[V];
+        unpack16<T, A>(__ldg(reinterpret_cast<const uint4*>(ys + pos * d) + c), yv);
+#pragma unroll
+        for (int u = 0; u < V; ++u) acc[u] = fma(wt, yv[u], acc[u]);
+      }
+      reinterpret_cast<uint4*>(y + i * d)[c] = pack16<T, A>(acc);
+    }
+  } else {
+    for (int64_t c = lane; c < d; c += 32) {
+      A acc = A(0);
+      for (int j = 0; j < k; ++j) {
+        const int64_t pos = __ldg(p.inverse_pos + i * k + j);
+        acc = fma((A)__ldg(w + i * k + j), (A)to_f(ys[pos * d + c]), acc);
+      }
+      if constexpr (std::is_same<T, double>::value)
+        y[i * d + c] = acc;
+      else
+        y[i * d + c] = from_f<T>((float)acc);
+    }
+  }
+}
+
+// ---------------------------------------------------------- scatter_backward
+template <typename T>
+__global__ void scatter_bwd_kernel(const T* __restrict__ d_xs, int64_t d, fmoe_plan p,
+                                   const T* __restrict__ addend, T* __restrict__ dx) {
+  using A = AccOf<T>;
+  constexpr int V = Vec<T>::N;
+  const int64_t i = warp_id_global();
+  const int lane = threadIdx.x & 31;
+  if (i >= p.n_b) return;
+  const int k = (int)p.k;
+  if ((d % V) == 0) {
+    const int64_t nv = d / V;
+    for (int64_t c = lane; c < nv; c += 32) {
+      A acc[V];
+#pragma unroll
+      for (int u = 0; u < V; ++u) acc[u] = A(0);
+      for (int j = 0; j < k; ++j) {
+        const int64_t pos = __ldg(p.inverse_pos + i * k + j);
+        A g[V];
+        unpack16<T, A>(__ldg(reinterpret_cast<const uint4*>(d_xs + pos * d) + c), g);
+#pragma unroll
+        for (int u = 0; u < V; ++u) acc[u] += g[u];
+      }
+      if (addend) {  // d_x += gate.d_x (moe_layer.cpp:140)
+        A g[V];
+        unpack16<T, A>(__ldg(reinterpret_cast<const uint4*>(addend + i * d) + c), g);
+#pragma unroll
+        for (int u = 0; u < V; ++u) acc[u] += g[u];
+      }
+      reinterpret_cast<uint4*>(dx + i * d)[c] = pack16<T, A>(acc);
+    }
+  } else {
+    for (int64_t c = lane; c < d; c += 32) {
+      A acc = A(0);
+      for (int j = 0; j < k; ++j) acc += (A)to_f(d_xs[(int64_t)__ldg(p.inverse_pos + i * k + j) * d + c]);
+      if (addend) acc += (A)to_f(addend[i * d + c]);
+      if constexpr (std::is_same<T, double>::value)
+        dx[i * d + c] = acc;
+      else
+        dx[i * d + c] = from_f<T>((float)acc);
+    }
+  }
+}
+
+// ---------------------------------------------------- gather_combine_backward
+// In-order dot product as the reference build computes it (see
+// oracle/fmoe_oracle.c dot_ref): paired products rounded and added in
+// order, a final odd term fused.
+template <typename A, typename T>
+__device__ __forceinline__ A dot_ref_seq(const T* a, const T* b, int64_t n) {
+  A dot = A(0);
+  const int64_t paired = n & ~int64_t(1);
+  for (int64_t c = 0; c < paired; ++c) {
+    const A prod = __dmul_rn((A)to_f(a[c]), (A)to_f(b[c]));
+    dot = __dadd_rn(dot, prod);
+  }
+  if (n & 1) dot = fma((A)to_f(a[paired]), (A)to_f(b[paired]), dot);
+  return dot;
+}
+
+template <typename T, typename S>
+__global__ void gcb_kernel(const T* __restrict__ dy, const T* __restrict__ ys, int64_t d, fmoe_plan p,
+                           const S* __restrict__ w, T* __restrict__ d_ys, S* __restrict__ d_w,
+                           const float* __restrict__ scores, const int32_t* __restrict__ topk_idx,
+                           __nv_bfloat16* __restrict__ dz) {
+  using A = AccOf<T>;
+  constexpr int V = Vec<T>::N;
+  const int64_t i = warp_id_global();
+  const int lane = threadIdx.x & 31;
+  const int k = (int)p.k;
+  if (i >= p.n_b) {
+    if (p.align <= 1) return;
+    const int64_t row = pad_row(p, i - p.n_b);
+    if (row < 0) return;
+    for (int64_t c = lane; c < d; c += 32) d_ys[row * d + c] = T(0);
+    return;
+  }
+  const T* dyr = dy + i * d;
+  float dw_f[8];
+  for (int j = 0; j < k; ++j) {
+    const int64_t pos = __ldg(p.inverse_pos + i * k + j);
+    const A wt = (A)__ldg(w + i * k + j);
+    T* dr = d_ys + pos * d;
+    const T* yr = ys + pos * d;
+    A part = A(0);
+    if ((d % V) == 0) {
+      const int64_t nv = d / V;
+      for (int64_t c = lane; c < nv; c += 32) {
+        A g[V], yv[V], o[V];
+        unpack16<T, A>(__ldg(reinterpret_cast<const uint4*>(dyr) + c), g);
+        unpack16<T, A>(__ldg(reinterpret_cast<const uint4*>(yr) + c), yv);
+#pragma unroll
+        for (int u = 0; u < V; ++u) {
+          if constexpr (std::is_same<T, double>::value)
+            o[u] = __dmul_rn(wt, g[u]);
+          else
+            o[u] = wt * g[u];
+          part = fma(g[u], yv[u], part);
+        }
+        reinterpret_cast<uint4*>(dr)[c] = pack16<T, A>(o);
+      }
+    } else {
+      for (int64_t c = lane; c < d; c += 32) {
+        const A g = (A)to_f(dyr[c]);
+        if constexpr (std::is_same<T, double>::value)
+          dr[c] = __dmul_rn(wt, g);
+        else
+          dr[c] = from_f<T>((float)(wt * g));
+        part = fma(g, (A)to_f(yr[c]), part);
+      }
+    }
+    A dot;
+    if constexpr (std::is_same<T, double>::value) {
+      dot = lane == 0 ? dot_ref_seq<A>(dyr, yr, d) : A(0);  // parity: reference order
+      (void)part;
+    } else {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      dot = part;
+    }
+    if (lane == 0) d_w[i * k + j] = (S)dot;
+    if (j < 8) dw_f[j] = (float)dot;
+  }
+  if (dz != nullptr) {
+    // Softmax Jacobian (gate.cpp:44-59) fused: ds is k-sparse.
+    const int E = (int)p.n_experts;
+    const float* s = scores + i * E;
+    int ix[8];
+    float dot = 0.f;
+    for (int j = 0; j < k && j < 8; ++j) {
+      ix[j] = __ldg(topk_idx + i * k + j);
+      dot = fmaf(dw_f[j], __ldg(s + ix[j]), dot);
+    }
+    for (int e = lane; e < E; e += 32) {
+      float dse = 0.f;
+      for (int j = 0; j < k && j < 8; ++j)
+        if (ix[j] == e) dse += dw_f[j];
+      dz[i * E + e] = __float2bfloat16_rn(__ldg(s + e) * (dse - dot));
+    }
+  }
+}
+
+// --------------------------------------------------------------- colsum
+template <typename T, typename O>
+__global__ void block_colsum_kernel(const T* __restrict__ src, int64_t n_cols,
+                                    const int32_t* __restrict__ offsets,
+                                    const int32_t* __restrict__ counts, O* __restrict__ out) {
+  const int g = blockIdx.y;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_cols) return;
+  const int64_t r0 = __ldg(offsets + g), n = __ldg(counts + g);
+  O acc = O(0);
+  const T* p = src + r0 * n_cols + c;
+  int64_t r = 0;
+  for (; r + 8 <= n; r += 8) {
+    T v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = p[(r + u) * n_cols];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += (O)to_f(v[u]);
+  }
+  for (; r < n; ++r) acc += (O)to_f(p[r * n_cols]);
+  out[(int64_t)g * n_cols + c] = acc;
+}
+
+}  // namespace
+
+void scatter(Ctx* ctx, fmoe_dtype t, const void* x, int64_t d, const fmoe_plan& p, void* xs) {
+  const int64_t warps = p.n_b + (p.align > 1 ? p.n_experts * 128 : 0);
+  if (warps == 0) return;
+  const unsigned grid = (unsigned)ceil_div(warps * 32, 256);
+  scatter_kernel<<<grid, 256, 0, ctx->stream>>>(reinterpret_cast<const uint8_t*>(x),
+                                                d * (int64_t)dtype_size(t), p,
+                                                reinterpret_cast<uint8_t*>(xs));
+  CK_LAUNCH(ctx);
+}
+
+void gather_combine(Ctx* ctx, fmoe_dtype t, const void* ys, int64_t d, const fmoe_plan& p,
+                    const void* w, void* y) {
+  if (p.n_b == 0) return;
+  const unsigned grid = (unsigned)ceil_div(p.n_b * 32, 256);
+  dispatch_dtype(t, [&](auto* tag) {
+    using T = std::remove_pointer_t<decltype(tag)>;
+    using S = typename ScoreOf<T>::type;
+    gather_combine_kernel<T, S><<<grid, 256, 0, ctx->stream>>>(
+        reinterpret_cast<const T*>(ys), d, p, reinterpret_cast<const S*>(w), reinterpret_cast<T*>(y));
+  });
+  CK_LAUNCH(ctx);
+}
+
+void scatter_bwd(Ctx* ctx, fmoe_dtype t, const void* d_xs, int64_t d, const fmoe_plan& p, void* dx,
+                 const void* addend) {
+  if (p.n_b == 0) return;
+  const unsigned grid = (unsigned)ceil_div(p.n_b * 32, 256);
+  dispatch_dtype(t, [&](auto* tag) {
+    using T = std::remove_pointer_t<decltype(tag)>;
+    scatter_bwd_kernel<T><<<grid, 256, 0, ctx->stream>>>(reinterpret_cast<const T*>(d_xs), d, p,
+                                                        reinterpret_cast<const T*>(addend),
+                                                        reinterpret_cast<T*>(dx));
+  });
+  CK_LAUNCH(ctx);
+}
+
+void gather_combine_bwd(Ctx* ctx, fmoe_dtype t, const void* dy, const void* ys, int64_t d,
+                        const fmoe_plan& p, const void* w, void* d_ys, void* d_w,
+                        const void* scores, const int32_t* topk_idx, __nv_bfloat16* dz) {
+  const int64_t warps = p.n_b + (p.align > 1 ? p.n_experts * 128 : 0);
+  if (warps == 0) return;
+  if (dz && p.k > 8) shape_error("fused gate backward supports k <= 8");
+  const unsigned grid = (unsigned)ceil_div(warps * 32, 256);
+  dispatch_dtype(t, [&](auto* tag) {
+    using T = std::remove_pointer_t<decltype(tag)>;
+    using S = typename ScoreOf<T>::type;
+    gcb_kernel<T, S><<<grid, 256, 0, ctx->stream>>>(
+        reinterpret_cast<const T*>(dy), reinterpret_cast<const T*>(ys), d, p,
+        reinterpret_cast<const S*>(w), reinterpret_cast<T*>(d_ys), reinterpret_cast<S*>(d_w),
+        reinterpret_cast<const float*>(scores), topk_idx, dz);
+  });
+  CK_LAUNCH(ctx);
+}
+
+void block_colsum(Ctx* ctx, fmoe_dtype t, const void* src, int64_t n_cols, const int32_t* offsets,
+                  const int32_t* counts, int64_t n_blocks, void* out) {
+  if (n_blocks == 0 || n_cols == 0) return;
+  dim3 grid((unsigned)ceil_div(n_cols, 128), (unsigned)n_blocks);
+  dispatch_dtype(t, [&](auto* tag) {
+    using T = std::remove_pointer_t<decltype(tag)>;
+    using O = typename ScoreOf<T>::type;  // f64 -> f64, else f32
+    block_colsum_kernel<T, O><<<grid, 128, 0, ctx->stream>>>(reinterpret_cast<const T*>(src), n_cols,
+                                                            offsets, counts, reinterpret_cast<O*>(out));
+  });
+  CK_LAUNCH(ctx);
+}
+
+}  // namespace fmoe_b200

@@ -1,0 +1,218 @@
+// plan.cu -- build_plan on device (dispatch.cpp:10-47): expert histogram,
+// exclusive scan (optionally 128-row aligned blocks) and the stable
+// (row, slot) position of every selection, without a global sort.
+//
+//   K2a plan_hist  : one warp per chunk of 512 flat selections f = i*k + j;
+//                    __match_any_sync-aggregated shared-memory histogram
+//                    -> chunk_hist[c][e]; out-of-range index -> error flag.
+//   K2b plan_scan  : one CTA.  counts[e] = sum_c chunk_hist[c][e]; aligned
+//                    exclusive scan -> offsets; per-chunk bases
+//                    base[c][e] = offsets[e] + sum_{c'<c} hist[c'][e];
+//                    padding rows (src_row = -1); 128-row tile -> expert table.
+//   K2c plan_rank  : re-walks each chunk in order; within a 32-wide step the
+//                    rank of a lane among equal experts is popc(match & lt),
+//                    across steps a per-warp shared counter carries it.  Hence
+//                    pos(f) = base[c][e] + #{f' < f in chunk c : idx[f'] = e},
+//                    exactly the reference's row-major fill order.
+// Integer-exact by construction; checked bit-for-bit against the oracle.
+#include "common.cuh"
+#include "plan.cuh"
+
+namespace fmoe_b200 {
+
+constexpr int kChunk = 512;       // selections per warp chunk
+constexpr int kWarpsPerCta = 4;
+
+__global__ void plan_hist(const int32_t* __restrict__ idx, int64_t nk, int n_experts,
+                          int32_t* __restrict__ chunk_hist, int* __restrict__ err) {
+  extern __shared__ int32_t sh[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int32_t* hist = sh + w * n_experts;
+  for (int e = lane; e < n_experts; e += 32) hist[e] = 0;
+  __syncwarp();
+  const int64_t chunk = (int64_t)blockIdx.x * kWarpsPerCta + w;
+  const int64_t f0 = chunk * kChunk;
+  if (f0 < nk) {
+    for (int s = 0; s < kChunk; s += 32) {
+      const int64_t f = f0 + s + lane;
+      int key = -1;
+      if (f < nk) {
+        key = __ldg(idx + f);
+        if (key < 0 || key >= n_experts) {
+          atomicExch(err, 1);
+          key = -1;
+        }
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      if (key >= 0 && (__ffs(peers) - 1) == lane) hist[key] += __popc(peers);
+      __syncwarp();
+    }
+    for (int e = lane; e < n_experts; e += 32) chunk_hist[chunk * n_experts + e] = hist[e];
+  }
+}
+
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// One CTA of 1024 threads.
+__global__ void plan_scan(int32_t* __restrict__ chunk_hist, int n_chunks, int n_experts, int align,
+                          int64_t capacity, int32_t* __restrict__ counts, int32_t* __restrict__ offsets,
+                          int32_t* __restrict__ src_row, int32_t* __restrict__ tile_expert,
+                          int32_t* __restrict__ n_tiles) {
+  extern __shared__ int32_t sh[];  // [n_experts] aligned counts, then scan scratch
+  int32_t* acnt = sh;
+  __shared__ int32_t warp_tot[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  // phase 1: per-expert totals (one warp per expert column, lanes over chunks)
+  for (int e = warp; e < n_experts; e += nwarps) {
+    int s = 0;
+    for (int c = lane; c < n_chunks; c += 32) s += chunk_hist[(int64_t)c * n_experts + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      counts[e] = s;
+      acnt[e] = (s + align - 1) / align * align;
+    }
+  }
+  __syncthreads();
+  // phase 2: exclusive scan of aligned counts (thread t owns a contiguous run)
+  const int per = (n_experts + blockDim.x - 1) / blockDim.x;
+  const int lo = threadIdx.x * per, hi = min(lo + per, n_experts);
+  int run = 0;
+  for (int e = lo; e < hi; ++e) run += acnt[e];
+  int incl = warp_incl_scan(run, lane);
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int v = lane < nwarps ? warp_tot[lane] : 0;
+    v = warp_incl_scan(v, lane);
+    warp_tot[lane] = v;
+  }
+  __syncthreads();
+  int base = incl - run + (warp > 0 ? warp_tot[warp - 1] : 0);
+  for (int e = lo; e < hi; ++e) {
+    const int a = acnt[e];
+    acnt[e] = base;  // now: exclusive offset
+    offsets[e] = base;
+    base += a;
+  }
+  if (threadIdx.x == blockDim.x - 1) {
+    offsets[n_experts] = base;
+    if (n_tiles) n_tiles[0] = base / 128;
+  }
+  __syncthreads();
+  // phase 3: chunk bases, padding rows, tile table
+  for (int e = warp; e < n_experts; e += nwarps) {
+    const int off = acnt[e];
+    // lanes own contiguous chunk ranges so the scan follows chunk order
+    const int cper = (n_chunks + 31) / 32;
+    const int c0 = lane * cper, c1 = min(c0 + cper, n_chunks);
+    int loc = 0;
+    for (int c = c0; c < c1; ++c) loc += chunk_hist[(int64_t)c * n_experts + e];
+    const int ex = warp_incl_scan(loc, lane) - loc;
+    int b = off + ex;
+    for (int c = c0; c < c1; ++c) {
+      const int h = chunk_hist[(int64_t)c * n_experts + e];
+      chunk_hist[(int64_t)c * n_experts + e] = b;
+      b += h;
+    }
+    const int cnt = counts[e];
+    const int next = (e + 1 < n_experts) ? -1 : 0;  // resolved below
+    (void)next;
+    const int end = off + (cnt + align - 1) / align * align;
+    for (int r = off + cnt + lane; r < end; r += 32) src_row[r] = -1;
+    if (tile_expert)
+      for (int t = off / 128 + lane; t < end / 128; t += 32) tile_expert[t] = e;
+  }
+  (void)capacity;
+}
+
+__global__ void plan_rank(const int32_t* __restrict__ idx, int64_t nk, int k, int n_experts,
+                          const int32_t* __restrict__ chunk_base, int32_t* __restrict__ src_row,
+                          int32_t* __restrict__ slot, int32_t* __restrict__ inverse_pos) {
+  extern __shared__ int32_t sh[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int32_t* run = sh + w * n_experts;
+  for (int e = lane; e < n_experts; e += 32) run[e] = 0;
+  __syncwarp();
+  const int64_t chunk = (int64_t)blockIdx.x * kWarpsPerCta + w;
+  const int64_t f0 = chunk * kChunk;
+  if (f0 >= nk) return;
+  const int32_t* base = chunk_base + chunk * n_experts;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int s = 0; s < kChunk; s += 32) {
+    const int64_t f = f0 + s + lane;
+    int key = -1;
+    if (f < nk) {
+      key = __ldg(idx + f);
+      if (key < 0 || key >= n_experts) key = -1;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    int before = 0;
+    if (key >= 0) before = run[key];
+    __syncwarp();
+    if (key >= 0) {
+      const int pos = __ldg(base + key) + before + __popc(peers & lt);
+      const int i = (int)(f / k);
+      src_row[pos] = i;
+      slot[pos] = (int)(f - (int64_t)i * k);
+      inverse_pos[f] = pos;
+      if ((__ffs(peers) - 1) == lane) run[key] = before + __popc(peers);
+    }
+    __syncwarp();
+  }
+}
+
+int64_t plan_capacity(int64_t n_b, int64_t k, int64_t n_experts, int64_t align) {
+  const int64_t nk = n_b * k;
+  if (align <= 1) return nk;
+  return ceil_div(nk + n_experts * (align - 1), align) * align;
+}
+
+int64_t plan_scratch_bytes(int64_t n_b, int64_t k, int64_t n_experts) {
+  const int64_t chunks = ceil_div(n_b * k, kChunk) + 1;
+  return chunks * n_experts * 4 + 256;
+}
+
+void plan_build(Ctx* ctx, const int32_t* topk_idx, const fmoe_plan& p) {
+  const int64_t nk = p.n_b * p.k;
+  const int E = (int)p.n_experts;
+  if (E < 1) shape_error("build_plan: need at least one expert");
+  if ((int64_t)E * kWarpsPerCta * 4 > 200 * 1024)
+    shape_error("build_plan: too many experts for the device plan (max 12800)");
+  if (p.align != 1 && p.align != 128) shape_error("build_plan: align must be 1 or 128");
+  if (nk > (int64_t)1 << 30) shape_error("build_plan: n_b*k too large");
+  const int64_t chunks = ceil_div(nk, kChunk);
+  int32_t* chunk_hist = reinterpret_cast<int32_t*>(p.scratch);
+  const size_t smem = (size_t)E * kWarpsPerCta * 4;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(plan_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(plan_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(plan_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  const unsigned grid = (unsigned)std::max<int64_t>(1, ceil_div(chunks, kWarpsPerCta));
+  if (nk > 0) {
+    plan_hist<<<grid, 32 * kWarpsPerCta, smem, ctx->stream>>>(topk_idx, nk, E, chunk_hist, ctx->d_error);
+    CK_LAUNCH(ctx);
+  }
+  plan_scan<<<1, 1024, (size_t)E * 4, ctx->stream>>>(chunk_hist, (int)chunks, E, (int)p.align,
+                                                     p.capacity, p.counts, p.offsets, p.src_row,
+                                                     p.align == 128 ? p.tile_expert : nullptr,
+                                                     p.n_tiles);
+  CK_LAUNCH(ctx);
+  if (nk > 0) {
+    plan_rank<<<grid, 32 * kWarpsPerCta, smem, ctx->stream>>>(topk_idx, nk, (int)p.k, E, chunk_hist,
+                                                              p.src_row, p.slot, p.inverse_pos);
+    CK_LAUNCH(ctx);
+  }
+}
+
+}  // namespace fmoe_b200

@@ -1,0 +1,89 @@
+// tc_gemm.cuh -- the grouped tcgen05/TMEM/TMA GEMM for sm_100a (bf16 in,
+// fp32 accumulate), shared by every dense contraction of the MoE layer:
+//
+//   gate logits + softmax + top-k   x[N,d] * Wg[d,E]                 (gate.cpp:30-33)
+//   expert fc1 + bias + relu        xs[rows,d] * W1_e[d,h]           (expert.cpp:30-31)
+//   expert fc2 + bias               H[rows,h] * W2_e[h,d]            (expert.cpp:32)
+//   dgrad fc2 * relu mask           dYs[rows,d] * W2_e^T             (expert.cpp:47-48)
+//   dgrad fc1                       dPre[rows,h] * W1_e^T            (expert.cpp:55)
+//   wgrad fc2 / fc1                 H_e^T dYs_e, xs_e^T dPre_e       (expert.cpp:42,50)
+//   gate dx + scatter_backward      dz[N,E] * Wg^T + sum_j d_xs[pos] (gate.cpp:63, dispatch.cpp:80-95)
+//   gate dWg (split-K partials)     x^T dz                           (gate.cpp:62)
+//
+// Design (SURVEY §7, B200 guide "Canonical Blackwell GEMM"):
+//   * persistent: grid = #SMs, static round-robin over tiles; the tile list
+//     is derived on device from the dispatch plan (no host sync);
+//   * warp-specialised, 256 threads: warp0 = TMA producer, warp1 = MMA issuer
+//     (one elected lane, tcgen05.mma.cta_group::1.kind::f16 M=128, N=BN, K=16),
+//     warp2 = TMEM allocator, warps 4..7 = epilogue (one TMEM lane = one row);
+//   * smem ring of STAGES x (A 128x64 + B BNx64) bf16, 128B-swizzled TMA
+//     boxes, full/empty mbarriers; 2 TMEM accumulators (2*BN fp32 columns)
+//     so the epilogue of tile i overlaps the MMAs of tile i+1;
+//   * operands may be K-major or MN-major (weights are used in their stored
+//     reference layout W1[d,h] / W2[h,d] for both the forward and the
+//     transposed backward products -- no materialised transposes);
+//   * two tile spaces: RAGGED_M (128-row tiles of the 128-aligned expanded
+//     buffer, each tile owned by one expert) and RAGGED_K (per-group K row
+//     ranges: the weight gradients, whose contraction runs over tokens).
+#pragma once
+
+#include <cuda.h>
+
+#include "common.cuh"
+
+namespace fmoe_b200 {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = one 128-byte swizzle row
+constexpr int NUM_THREADS = 256;
+
+enum Mode : int { RAGGED_M = 0, RAGGED_K = 1 };
+enum Epi : int {
+  EPI_BF16 = 0,       // C = bf16(acc [+ bias] [relu])
+  EPI_MASK_BF16 = 1,  // C = bf16(acc * (mask > 0))           dgrad fc2 (relu_backward, strict >)
+  EPI_F32 = 2,        // C = acc (fp32)                         weight gradients
+  EPI_GATE = 3,       // softmax + top-k over the row           gate forward
+  EPI_GATE_DX = 4,    // C = bf16(sum_j d_xs[pos(i,j)] + acc)   scatter_backward + gate d_x
+};
+
+struct Params {
+  int mode;
+  int M, N, K;               // RAGGED_M: M = rows (tensor extent), K = contraction
+  int n_groups;              // RAGGED_K: number of groups
+  const int* tile_group;     // RAGGED_M: group of each 128-row tile (NULL: all group 0)
+  const int* n_mtiles;       // RAGGED_M: device count of valid row tiles (NULL: ceil(M/128))
+  const int* k_offsets;      // RAGGED_K: [G+1] K-row range of each group (multiples of 64)
+  int b_group_rows;          // RAGGED_M: rows of the 2-D B tensor per group
+  // epilogue
+  int epi;
+  void* C;
+  int64_t ldc;
+  int64_t c_group_stride;    // RAGGED_K: elements between groups' outputs
+  const float* bias;         // [G][N] fp32 or NULL
+  int64_t bias_group_stride;
+  int relu;
+  const __nv_bfloat16* mask; // EPI_MASK_BF16: [rows][ldm]
+  int64_t ldm;
+  // EPI_GATE
+  float* scores;             // [M][N]
+  int* topk_idx;             // [M][topk]
+  float* topk_val;
+  int topk;                  // <= 8 fused; 0 = scores only
+  // EPI_GATE_DX
+  const __nv_bfloat16* gather_src;  // d_xs [rows][N]
+  const int* inverse_pos;           // [M][gk]
+  int gk;
+};
+
+// Host: build a 2-D bf16 tensor map over a row-major [outer, inner] matrix
+// with a (box_inner x box_outer) box, 128B swizzle, zero OOB fill.
+CUtensorMap make_tmap(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                      uint32_t box_inner, uint32_t box_outer);
+
+// Host: launch.  a_mn / b_mn select MN-major operands; bn in {64,128,256}.
+void launch(Ctx* ctx, int bn, bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
+            const Params& p, int64_t max_tiles);
+
+}  // namespace tc
+}  // namespace fmoe_b200
