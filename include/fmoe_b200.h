@@ -200,10 +200,53 @@ int fmoe_layer_step_host(fmoe_layer* layer, const void* x_host, const void* dy_h
                          void* y_host, void* dx_host);
 
 /* --------------------------------------------- expert parallelism (L2, EP) */
-/* Communicator over NCCL (NVLink/NVSwitch).  Rank 0 creates an id, the host
- * broadcasts it out of band (torch.distributed store, MPI, ...). */
+/* A context's transport replaces the reference's Transport (transport.hpp:18-38).
+ * Communicator over NCCL (NVLink/NVSwitch), one process per GPU: rank 0
+ * creates a 128-byte id, the host broadcasts it out of band (torch.distributed
+ * store, MPI, ...), every rank calls fmoe_comm_init.  TransportError on
+ * failure. */
 int fmoe_comm_unique_id(void* id_out, int64_t id_bytes);
 int fmoe_comm_init(fmoe_ctx* ctx, const void* id, int64_t id_bytes, int world, int rank);
+/* In-process world (InProcWorld, transport.hpp:40-60): `world` ranks run as
+ * host threads of one process, each with its own context joined to the world
+ * (possibly all on one device).  Used to test the EP path on one GPU. */
+typedef struct fmoe_world fmoe_world;
+int fmoe_world_create(int world, fmoe_world** out);
+int fmoe_world_destroy(fmoe_world* world);
+int fmoe_ctx_join_world(fmoe_ctx* ctx, fmoe_world* world, int rank);
+
+/* ExchangePlan (collectives.hpp:16-33), host arrays of world*local_experts
+ * entries owned by the caller: send_counts[dest][local expert],
+ * recv_counts[source][local expert]. */
+typedef struct {
+  int64_t world, rank, local_experts;
+  int64_t* send_counts;
+  int64_t* recv_counts;
+  int64_t send_total, recv_total;
+} fmoe_exchange_plan;
+/* exchange_counts (collectives.hpp:39-40; collectives.cpp:69-109): collective
+ * over the context's transport; local_counts is this rank's per-global-expert
+ * row count (host, n_counts = world*local_experts).  Synchronises.  ShapeError
+ * when n_counts is not divisible by the world size. */
+int fmoe_exchange_counts(fmoe_ctx* ctx, const int64_t* local_counts, int64_t n_counts,
+                         fmoe_exchange_plan* plan);
+/* all_to_all_rows (collectives.hpp:41-47; collectives.cpp:146-203): rows grouped
+ * by (dest rank, dest local expert, scatter order) -> rows grouped by (local
+ * expert, source rank, source order), device buffers, stream-ordered. */
+int fmoe_a2a_rows(fmoe_ctx* ctx, fmoe_dtype dtype, const void* xs, int64_t d,
+                  const fmoe_exchange_plan* plan, void* out);
+/* Host-only layout of one exchange (no device work): send_off[E] (first row of
+ * each (dest rank, its local expert) chunk in the send layout,
+ * send_section_offsets collectives.cpp:114-122), chunk_off[el*W] (first row of
+ * (local expert e, source s) in the receive layout, recv_chunk_offsets
+ * collectives.cpp:126-135, index e*W+s), block_off[el+1] and rows[el] (expert
+ * blocks starting on `align`-row boundaries; align 1 = reference layout). */
+int fmoe_ep_layout(int world, int64_t local_experts, int64_t align, const int64_t* send_counts,
+                   const int64_t* recv_counts, int64_t* send_off, int64_t* chunk_off, int64_t* block_off,
+                   int64_t* rows);
+/* all_to_all_rows_reverse (collectives.hpp:48-50; collectives.cpp:205-265). */
+int fmoe_a2a_rows_reverse(fmoe_ctx* ctx, fmoe_dtype dtype, const void* ys, int64_t d,
+                          const fmoe_exchange_plan* plan, void* out);
 
 #ifdef __cplusplus
 }

@@ -286,6 +286,21 @@ class Orc(_Lib):
         self.call("orc_exchange_counts", lc, world, total, out)
         return out
 
+    def all_to_all_rows(self, send_bufs, local_counts, rank):
+        """collectives.cpp:146-203 for `rank`, given every rank's send buffer."""
+        lc = _arr(local_counts, np.int64)
+        world, total = lc.shape
+        bufs = [_arr(b, np.float64) for b in send_bufs]
+        d = bufs[0].shape[1]
+        el = total // world
+        rows = int(sum(lc[s, rank * el:(rank + 1) * el].sum() for s in range(world)))
+        out = np.empty((rows, d))
+        ptrs = (C.c_void_p * world)(*[b.ctypes.data for b in bufs])
+        f = self.lib.orc_all_to_all_rows
+        f.restype = None
+        f(ptrs, _ptr(lc), _i64(world), _i64(total), _i64(rank), _i64(d), _ptr(out))
+        return out
+
 
 class Ref(_Lib):
     """The reference compiled from /root/reference/proj/src (namespace fmoe_ref)."""

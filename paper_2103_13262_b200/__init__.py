@@ -29,5 +29,11 @@ from .api import (  # noqa: F401
     scatter,
     scatter_backward,
     version,
+    World,
+    ExchangePlan,
+    exchange_counts,
+    all_to_all_rows,
+    all_to_all_rows_reverse,
+    ep_layout,
 )
 from ._lib import LIB_PATH  # noqa: F401

@@ -75,8 +75,15 @@ EXPORTS = [
     "fmoe_gather_combine_bwd", "fmoe_experts_fwd", "fmoe_experts_bwd", "fmoe_layer_create",
     "fmoe_layer_destroy", "fmoe_layer_init_weights", "fmoe_layer_params", "fmoe_layer_grads",
     "fmoe_layer_routing", "fmoe_layer_fwd", "fmoe_layer_bwd", "fmoe_layer_step_host",
-    "fmoe_comm_unique_id", "fmoe_comm_init",
+    "fmoe_comm_unique_id", "fmoe_comm_init", "fmoe_world_create", "fmoe_world_destroy",
+    "fmoe_ctx_join_world", "fmoe_exchange_counts", "fmoe_ep_layout", "fmoe_a2a_rows",
+    "fmoe_a2a_rows_reverse",
 ]
+
+
+class ExchangePlanC(C.Structure):
+    _fields_ = [("world", i64), ("rank", i64), ("local_experts", i64), ("send_counts", vp),
+                ("recv_counts", vp), ("send_total", i64), ("recv_total", i64)]
 
 
 def _load():
@@ -115,6 +122,13 @@ def _load():
         "fmoe_layer_routing": [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(Plan)],
         "fmoe_layer_fwd": [vp, vp, vp],
         "fmoe_layer_bwd": [vp, vp, vp],
+        "fmoe_world_create": [C.c_int, C.POINTER(vp)],
+        "fmoe_world_destroy": [vp],
+        "fmoe_ctx_join_world": [vp, vp, C.c_int],
+        "fmoe_exchange_counts": [vp, vp, i64, C.POINTER(ExchangePlanC)],
+        "fmoe_ep_layout": [C.c_int, i64, i64, vp, vp, vp, vp, vp, vp],
+        "fmoe_a2a_rows": [vp, C.c_int, vp, i64, C.POINTER(ExchangePlanC), vp],
+        "fmoe_a2a_rows_reverse": [vp, C.c_int, vp, i64, C.POINTER(ExchangePlanC), vp],
         "fmoe_layer_step_host": [vp, vp, vp, vp, vp],
         "fmoe_comm_unique_id": [vp, i64],
         "fmoe_comm_init": [vp, vp, i64, C.c_int, C.c_int],

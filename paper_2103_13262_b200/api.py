@@ -78,6 +78,115 @@ class Context:
     def check(self):
         check(lib.fmoe_ctx_check(self.h))
 
+    def use_current_stream(self):
+        check(lib.fmoe_ctx_set_stream(self.h, C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)))
+        return self
+
+    def join_world(self, world: "World", rank: int):
+        """In-process expert-parallel world (InProcWorld analogue, one host thread per rank)."""
+        check(lib.fmoe_ctx_join_world(self.h, world.h, rank))
+
+    def init_nccl(self, dist, world: int, rank: int):
+        """NCCL communicator over NVLink; the 128-byte id travels through torch.distributed."""
+        buf = (C.c_char * 128)()
+        if rank == 0:
+            check(lib.fmoe_comm_unique_id(buf, 128))
+        obj = [bytes(buf)]
+        dist.broadcast_object_list(obj, src=0)
+        idb = (C.c_char * 128).from_buffer_copy(obj[0])
+        check(lib.fmoe_comm_init(self.h, idb, 128, world, rank))
+
+
+class World:
+    """fmoe_world: `world` ranks of one process (tests, single-GPU EP runs)."""
+
+    def __init__(self, world: int):
+        h = C.c_void_p()
+        check(lib.fmoe_world_create(world, C.byref(h)))
+        self.h, self.world = h, world
+
+    def __del__(self):
+        if getattr(self, "h", None) is not None and lib is not None:
+            lib.fmoe_world_destroy(self.h)
+            self.h = None
+
+
+# ----------------------------------------------------- EP collectives (L2)
+@dataclass
+class ExchangePlan:
+    """ExchangePlan (collectives.hpp:16-33)."""
+
+    rank: int
+    world: int
+    local_experts: int
+    send_counts: "np.ndarray"  # [world, local_experts]
+    recv_counts: "np.ndarray"  # [world, local_experts]
+    send_total: int
+    recv_total: int
+
+    def local_expert_rows(self):
+        return self.recv_counts.sum(axis=0)
+
+    def c(self):
+        import numpy as np
+
+        self._s = np.ascontiguousarray(self.send_counts.reshape(-1), dtype=np.int64)
+        self._r = np.ascontiguousarray(self.recv_counts.reshape(-1), dtype=np.int64)
+        return _lib.ExchangePlanC(self.world, self.rank, self.local_experts, self._s.ctypes.data,
+                                  self._r.ctypes.data, self.send_total, self.recv_total)
+
+
+def exchange_counts(local_counts, ctx: Context) -> ExchangePlan:
+    """exchange_counts (collectives.hpp:39-40) over ctx's transport."""
+    import numpy as np
+
+    lc = np.ascontiguousarray(np.asarray(local_counts, dtype=np.int64).reshape(-1))
+    s = np.zeros_like(lc)
+    r = np.zeros_like(lc)
+    p = _lib.ExchangePlanC(0, 0, 0, s.ctypes.data, r.ctypes.data, 0, 0)
+    check(lib.fmoe_exchange_counts(ctx.h, lc.ctypes.data, lc.size, C.byref(p)))
+    w, el = p.world, p.local_experts
+    return ExchangePlan(p.rank, w, el, s.reshape(w, el), r.reshape(w, el), p.send_total, p.recv_total)
+
+
+def all_to_all_rows(xs: torch.Tensor, plan: ExchangePlan, ctx: Context) -> torch.Tensor:
+    """all_to_all_rows (collectives.hpp:41-47)."""
+    xs = _dev(xs)
+    if xs.shape[0] != plan.send_total:
+        raise ProtocolError(f"all_to_all_rows: input rows {xs.shape[0]} != planned send total {plan.send_total}")
+    out = torch.empty(plan.recv_total, xs.shape[1], dtype=xs.dtype, device=xs.device)
+    pc = plan.c()
+    check(lib.fmoe_a2a_rows(ctx.h, dtype_code(xs.dtype), _p(xs), xs.shape[1], C.byref(pc), _p(out)))
+    return out
+
+
+def all_to_all_rows_reverse(ys: torch.Tensor, plan: ExchangePlan, ctx: Context) -> torch.Tensor:
+    """all_to_all_rows_reverse (collectives.hpp:48-50)."""
+    ys = _dev(ys)
+    if ys.shape[0] != plan.recv_total:
+        raise ProtocolError(f"all_to_all_rows_reverse: input rows {ys.shape[0]} != planned recv total")
+    out = torch.empty(plan.send_total, ys.shape[1], dtype=ys.dtype, device=ys.device)
+    pc = plan.c()
+    check(lib.fmoe_a2a_rows_reverse(ctx.h, dtype_code(ys.dtype), _p(ys), ys.shape[1], C.byref(pc), _p(out)))
+    return out
+
+
+def ep_layout(world: int, local_experts: int, align: int, send_counts, recv_counts):
+    """Host layout of one exchange through the library (fmoe_ep_layout):
+    (send_off [E], chunk_off [el, W], block_off [el+1], rows [el])."""
+    import numpy as np
+
+    e = world * local_experts
+    s = np.ascontiguousarray(np.asarray(send_counts, np.int64).reshape(-1))
+    r = np.ascontiguousarray(np.asarray(recv_counts, np.int64).reshape(-1))
+    so = np.zeros(e, np.int64)
+    co = np.zeros(e, np.int64)
+    bo = np.zeros(local_experts + 1, np.int64)
+    rows = np.zeros(local_experts, np.int64)
+    check(lib.fmoe_ep_layout(world, local_experts, align, s.ctypes.data, r.ctypes.data, so.ctypes.data,
+                             co.ctypes.data, bo.ctypes.data, rows.ctypes.data))
+    return so, co.reshape(local_experts, world), bo, rows
+
 
 def _ctx(t: torch.Tensor) -> Context:
     return Context.get(t.device)
@@ -320,13 +429,16 @@ class MoELayer:
     exposed as torch views; activations are cached inside the layer."""
 
     def __init__(self, config: MoEConfig, rank: int = 0, dtype: torch.dtype = torch.bfloat16,
-                 device=None, init: bool = True):
+                 device=None, init: bool = True, ctx: Optional[Context] = None):
         self.config = config
         self.rank = rank
         self.dtype = dtype
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
         self.device = dev
-        self.ctx = Context.get(dev)
+        # each layer owns a context (its stream and, under EP, its transport)
+        self.ctx = (ctx if ctx is not None else Context(dev.index)).use_current_stream()
         cfg = LayerConfig(config.n_b, config.d_m, config.d_h, config.k, config.n_e_local,
                           config.world_size, rank, config.seed, dtype_code(dtype))
         h = C.c_void_p()
@@ -345,6 +457,15 @@ class MoELayer:
     def init_weights(self):
         """init_state (moe_layer.cpp:28-45): the reference's generators."""
         check(lib.fmoe_layer_init_weights(self.h))
+
+    def connect(self, dist):
+        """Expert parallelism over NCCL: one process per GPU, torch.distributed
+        carries the communicator id (world/rank from the layer's config)."""
+        self.ctx.init_nccl(dist, self.config.world_size, self.rank)
+
+    def join(self, world: World):
+        """Expert parallelism inside one process (one host thread per rank)."""
+        self.ctx.join_world(world, self.rank)
 
     def _views(self):
         c = self.config
@@ -387,7 +508,7 @@ class MoELayer:
             raise ShapeError(f"forward: expected x [{self.config.n_b}, {self.config.d_m}] {self.dtype}")
         if y is None:
             y = torch.empty_like(x)
-        Context.get(self.device)
+        self.ctx.use_current_stream()
         check(lib.fmoe_layer_fwd(self.h, _p(x), _p(y)))
         self._x = x
         return y
@@ -398,14 +519,14 @@ class MoELayer:
         dy = _dev(dy)
         if dx is None:
             dx = torch.empty_like(dy)
-        Context.get(self.device)
+        self.ctx.use_current_stream()
         check(lib.fmoe_layer_bwd(self.h, _p(dy), _p(dx)))
         return dx
 
     def step_host(self, x_host: torch.Tensor, dy_host: Optional[torch.Tensor], y_host: torch.Tensor,
                   dx_host: Optional[torch.Tensor] = None):
         """Host-buffer forward(+backward) through fmoe_layer_step_host."""
-        Context.get(self.device)
+        self.ctx.use_current_stream()
         check(lib.fmoe_layer_step_host(self.h, _p(x_host), _p(dy_host), _p(y_host), _p(dx_host)))
 
 

@@ -260,8 +260,11 @@ int fmoe_experts_bwd(fmoe_ctx* ctx, fmoe_dtype dtype, const fmoe_plan* blocks, i
   FMOE_GUARD({
     check_plan(blocks);
     Ctx* c = C(ctx);
-    void* d_pre = ctx_workspace(c, (size_t)(blocks->capacity * d_h) * dtype_size(dtype) + 256);
-    experts_bwd(c, dtype, *blocks, d_m, d_h, params, xs, hidden, d_ys, d_xs, grads, d_pre);
+    const size_t pre_bytes = ((size_t)(blocks->capacity * d_h) * dtype_size(dtype) + 255) / 256 * 256;
+    uint8_t* ws = (uint8_t*)ctx_workspace(
+        c, pre_bytes + (size_t)experts_bwd_part_floats(*blocks, d_m, d_h) * 4 + 256);
+    experts_bwd(c, dtype, *blocks, d_m, d_h, params, xs, hidden, d_ys, d_xs, grads, ws,
+                (float*)(ws + pre_bytes));
   })
 }
 

@@ -56,7 +56,8 @@ struct Ctx {
   int num_sms = 148;
   int64_t launches = 0;
   int* d_error = nullptr;  // deferred device-side error flag (plan validation)
-  void* comm = nullptr;    // ncclComm_t when EP is initialised
+  struct Transport* transport = nullptr;  // EP exchange (comm.cuh); owned
+  bool owns_transport = true;
   void* ws = nullptr;      // grow-only scratch for operator-level calls
   size_t ws_size = 0;
   int world = 1, rank = 0;

@@ -1,29 +1,445 @@
-// ep.cu -- expert parallelism over NCCL (collectives.cpp:69-265).
-// Not wired yet: the single-GPU layer is the round-1 target; EP entry points
-// report a ProtocolError until fmoe_comm_init has been implemented.
+// ep.cu -- expert parallelism (moe_layer.cpp:85-91, 124-128; collectives.cpp:69-265).
+//
+// Rank r owns experts g in [r*el, (r+1)*el) (moe_layer.hpp:29-30).  Per step:
+//   forward : gate -> send plan over all E experts (reference layout: grouped by
+//             destination rank, then its local expert, then scatter order) ->
+//             scatter -> count exchange (C1) -> ONE host sync for the counts ->
+//             token exchange (C2, global_scatter) into the receive layout
+//             (local expert, source rank, source order) with 128-row aligned
+//             expert blocks -> grouped tcgen05 experts -> reverse exchange
+//             (C3, global_gather) -> gather_combine.
+//   backward: gather_combine_bwd -> C2 on d_ys -> experts backward -> C3 on
+//             d_xs -> gate backward fused with scatter_backward.
+// The plan of the forward is reused by the backward without a recount
+// (collectives.hpp:48-50).  Chunks are exchanged per (peer, local expert)
+// straight into their final slots, so the receive side needs no permute.
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "comm.cuh"
 #include "layer.cuh"
+#include "ops.cuh"
 
 namespace fmoe_b200 {
 
-struct Layer::Ep {};
+struct Layer::Ep {
+  int W = 1, r = 0;
+  int64_t el = 0, align = 1, cap_recv = 0;
+  // receive-side block plan (device) + host mirrors
+  fmoe_plan rplan{};
+  int32_t* d_recv_counts = nullptr;  // [W*el] rows from source s for local expert e
+  int32_t* h_pinned = nullptr;       // staging: send counts, recv counts, plan upload
+  std::vector<int64_t> h_send, h_recv, send_off, chunk_off, block_off, rows;
+  // receive-space activations
+  void *xs = nullptr, *hidden = nullptr, *ys = nullptr, *d_ys = nullptr, *d_pre = nullptr, *d_xs = nullptr;
+  bool planned = false;
+};
 
-void Layer::ep_alloc() {}
-void Layer::ep_forward(const void*, void*) {
-  protocol_error("forward: expert parallelism needs fmoe_comm_init (not available in this build)");
+namespace {
+void* alloc(std::vector<void*>& owned, int64_t bytes) {
+  void* p = nullptr;
+  CK(cudaMalloc(&p, std::max<int64_t>(bytes, 256)));
+  owned.push_back(p);
+  return p;
 }
-void Layer::ep_backward(const void*, void*) {
-  protocol_error("backward: expert parallelism needs fmoe_comm_init (not available in this build)");
+}  // namespace
+
+void Layer::ep_alloc() {
+  ep = new Ep;
+  Ep& P = *ep;
+  P.W = (int)cfg.world_size;
+  P.r = (int)cfg.rank;
+  P.el = cfg.n_e_local;
+  P.align = t == FMOE_BF16 ? 128 : 1;
+  // worst case: every token of every rank picks this rank's experts
+  P.cap_recv = plan_capacity(cfg.n_b * cfg.world_size, cfg.k, P.el, P.align);
+  const int64_t d = cfg.d_m, h = cfg.d_h, cap = P.cap_recv;
+  P.rplan.n_b = 0;
+  P.rplan.k = 1;
+  P.rplan.n_experts = P.el;
+  P.rplan.align = P.align;
+  P.rplan.capacity = cap;
+  P.rplan.counts = (int32_t*)alloc(owned, P.el * 4);
+  P.rplan.offsets = (int32_t*)alloc(owned, (P.el + 1) * 4);
+  P.rplan.tile_expert = (int32_t*)alloc(owned, (cap / 128 + 2) * 4);
+  P.rplan.n_tiles = (int32_t*)alloc(owned, 4);
+  P.d_recv_counts = (int32_t*)alloc(owned, P.W * P.el * 4);
+  const int64_t staging = E + P.W * P.el + (P.el + 1) + P.el + cap / 128 + 8;
+  CK(cudaMallocHost(&P.h_pinned, staging * 4));
+  h_stage = P.h_pinned;
+  P.xs = alloc(owned, cap * d * es);
+  P.hidden = alloc(owned, cap * h * es);
+  P.ys = alloc(owned, cap * d * es);
+  P.d_ys = alloc(owned, cap * d * es);
+  P.d_pre = alloc(owned, cap * h * es);
+  P.d_xs = alloc(owned, cap * d * es);
+  tpart = (float*)alloc(owned, experts_bwd_part_floats(P.rplan, d, h) * 4);
+}
+
+namespace {
+
+Transport* need_transport(Ctx* ctx, const fmoe_layer_config& cfg) {
+  Transport* tr = ctx->transport;
+  if (!tr)
+    protocol_error("forward: expert-parallel layer (world " + std::to_string(cfg.world_size) +
+                   ") needs a transport: fmoe_comm_init or fmoe_ctx_join_world");
+  if (tr->world != cfg.world_size) protocol_error("forward: transport world != config world");
+  if (tr->rank != cfg.rank) protocol_error("forward: transport rank != layer rank");
+  return tr;
+}
+
+// Grouped exchange of row chunks between the send layout (per destination
+// rank, per its local expert) and the receive layout (per local expert, per
+// source rank).  forward: send -> recv (all_to_all_rows); reverse: recv ->
+// send (all_to_all_rows_reverse).
+void exchange_rows(Ctx* ctx, Transport* tr, const Layer::Ep& P, size_t rb, const void* src, void* dst,
+                   bool forward) {
+  const int W = P.W, r = P.r;
+  const int64_t el = P.el;
+  const uint8_t* s8 = static_cast<const uint8_t*>(src);
+  uint8_t* d8 = static_cast<uint8_t*>(dst);
+  std::vector<Xfer> sends, recvs;
+  for (int p = 0; p < W; ++p) {
+    for (int64_t e = 0; e < el; ++e) {
+      const int64_t g = (int64_t)p * el + e;
+      const size_t send_rows = (size_t)P.h_send[g];        // rows this rank routes to (p, e)
+      const size_t recv_rows = (size_t)P.h_recv[g];        // rows rank p routes to my expert e
+      const int64_t so = P.send_off[g];
+      const int64_t ro = P.chunk_off[e * W + p];
+      if (p == r) {  // self rows bypass the transport (collectives.cpp:160-171)
+        if (send_rows != recv_rows) protocol_error("exchange: self counts disagree");
+        if (!send_rows) continue;
+        if (forward)
+          CK(cudaMemcpyAsync(d8 + ro * rb, s8 + so * rb, send_rows * rb, cudaMemcpyDeviceToDevice, ctx->stream));
+        else
+          CK(cudaMemcpyAsync(d8 + so * rb, s8 + ro * rb, send_rows * rb, cudaMemcpyDeviceToDevice, ctx->stream));
+        continue;
+      }
+      if (forward) {
+        sends.push_back({p, const_cast<uint8_t*>(s8) + so * rb, send_rows * rb});
+        recvs.push_back({p, d8 + ro * rb, recv_rows * rb});
+      } else {
+        sends.push_back({p, const_cast<uint8_t*>(s8) + ro * rb, recv_rows * rb});
+        recvs.push_back({p, d8 + so * rb, send_rows * rb});
+      }
+    }
+  }
+  tr->group(ctx, sends, recvs);
+}
+
+void zero_pads(Ctx* ctx, const Layer::Ep& P, size_t rb, void* buf) {
+  uint8_t* b = static_cast<uint8_t*>(buf);
+  for (int64_t e = 0; e < P.el; ++e) {
+    const int64_t a = P.block_off[e] + P.rows[e], z = P.block_off[e + 1];
+    if (z > a) CK(cudaMemsetAsync(b + a * rb, 0, (size_t)(z - a) * rb, ctx->stream));
+  }
+}
+
+}  // namespace
+
+// Host layout of one exchange (pure host arithmetic, exported as
+// fmoe_ep_layout so the multi-process CPU tests can drive it):
+//   send_off[g]          first row of (dest rank g/el, its local expert g%el) in the
+//                        send layout = exclusive prefix of send counts
+//                        (send_section_offsets, collectives.cpp:114-122)
+//   chunk_off[e*W + s]   first row of (local expert e, source s) in the receive
+//                        layout (recv_chunk_offsets, collectives.cpp:126-135),
+//                        expert blocks starting on `align`-row boundaries
+//   block_off[e], rows[e] expert block start (el+1 entries) and valid rows.
+void ep_layout(int W, int64_t el, int64_t align, const int64_t* send, const int64_t* recv,
+               int64_t* send_off, int64_t* chunk_off, int64_t* block_off, int64_t* rows) {
+  const int64_t E = (int64_t)W * el;
+  if (E > 0) send_off[0] = 0;
+  for (int64_t g = 1; g < E; ++g) send_off[g] = send_off[g - 1] + send[g - 1];
+  int64_t at = 0;
+  for (int64_t e = 0; e < el; ++e) {
+    block_off[e] = at;
+    int64_t c = at;
+    for (int s = 0; s < W; ++s) {
+      chunk_off[e * W + s] = c;
+      c += recv[(int64_t)s * el + e];
+    }
+    rows[e] = c - at;
+    at += (rows[e] + align - 1) / align * align;
+  }
+  block_off[el] = at;
+}
+
+// exchange_counts (collectives.cpp:69-109) + the receive layout
+// (recv_chunk_offsets, collectives.cpp:126-135) with aligned expert blocks.
+static void ep_plan(Layer& L, Transport* tr) {
+  Ctx* ctx = L.ctx;
+  Layer::Ep& P = *L.ep;
+  const int W = P.W, r = P.r;
+  const int64_t el = P.el, E = L.E;
+  std::vector<Xfer> sends, recvs;
+  for (int p = 0; p < W; ++p) {
+    if (p == r) continue;
+    sends.push_back({p, L.plan.counts + p * el, (size_t)el * 4});
+    recvs.push_back({p, P.d_recv_counts + p * el, (size_t)el * 4});
+  }
+  CK(cudaMemcpyAsync(P.d_recv_counts + r * el, L.plan.counts + r * el, el * 4, cudaMemcpyDeviceToDevice,
+                     ctx->stream));
+  tr->group(ctx, sends, recvs);
+  int32_t* hs = P.h_pinned;
+  int32_t* hr = hs + E;
+  CK(cudaMemcpyAsync(hs, L.plan.counts, E * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(hr, P.d_recv_counts, W * el * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));  // the one host sync of an EP step
+  P.h_send.assign(hs, hs + E);
+  P.h_recv.assign(hr, hr + W * el);
+  P.send_off.assign(E, 0);
+  P.rows.assign(el, 0);
+  P.block_off.assign(el + 1, 0);
+  P.chunk_off.assign(el * W, 0);
+  ep_layout(W, el, P.align, P.h_send.data(), P.h_recv.data(), P.send_off.data(), P.chunk_off.data(),
+            P.block_off.data(), P.rows.data());
+  const int64_t at = P.block_off[el];
+  if (at > P.cap_recv) protocol_error("exchange: received rows exceed the layer capacity");
+  // upload the receive block plan (counts, offsets, 128-row tile table)
+  int32_t* up = hr + W * el;
+  for (int64_t e = 0; e < el; ++e) up[e] = (int32_t)P.rows[e];
+  int32_t* uo = up + el;
+  for (int64_t e = 0; e <= el; ++e) uo[e] = (int32_t)P.block_off[e];
+  int32_t* ut = uo + el + 1;
+  int64_t nt = 0;
+  if (P.align == 128) {
+    for (int64_t e = 0; e < el; ++e)
+      for (int64_t tt = P.block_off[e] / 128; tt < P.block_off[e + 1] / 128; ++tt) ut[nt++] = (int32_t)e;
+  }
+  ut[nt] = (int32_t)nt;  // n_tiles rides at the end
+  CK(cudaMemcpyAsync(P.rplan.counts, up, el * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(P.rplan.offsets, uo, (el + 1) * 4, cudaMemcpyHostToDevice, ctx->stream));
+  if (nt) CK(cudaMemcpyAsync(P.rplan.tile_expert, ut, nt * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(P.rplan.n_tiles, ut + nt, 4, cudaMemcpyHostToDevice, ctx->stream));
+  P.planned = true;
+}
+
+void Layer::ep_forward(const void* x, void* y) {
+  Transport* tr = need_transport(ctx, cfg);
+  Ep& P = *ep;
+  const int64_t d = cfg.d_m, h = cfg.d_h;
+  const size_t rb = (size_t)d * es;
+  plan_build(ctx, idx, plan);                  // send plan over all E experts, reference layout
+  scatter(ctx, t, x, d, plan, xs);
+  ep_plan(*this, tr);                          // C1 + receive layout
+  ctx_mark(ctx, MARK_PLAN);
+  zero_pads(ctx, P, rb, P.xs);
+  exchange_rows(ctx, tr, P, rb, xs, P.xs, true);   // C2 global_scatter
+  ctx_mark(ctx, MARK_SCATTER);
+  experts_fwd(ctx, t, P.rplan, d, h, params(), P.xs, P.hidden, P.ys);
+  exchange_rows(ctx, tr, P, rb, P.ys, ys, false);  // C3 global_gather
+  gather_combine(ctx, t, ys, d, plan, vals, y);
+  ctx_mark(ctx, MARK_GATHER);
+}
+
+void Layer::ep_backward(const void* dy, void* dx) {
+  Transport* tr = need_transport(ctx, cfg);
+  Ep& P = *ep;
+  if (!P.planned) protocol_error("backward: no expert-parallel forward cache");
+  const int64_t n = cfg.n_b, d = cfg.d_m, h = cfg.d_h, k = cfg.k;
+  const size_t rb = (size_t)d * es;
+  const bool bf = t == FMOE_BF16;
+  ctx_mark(ctx, MARK_BWD_BEGIN);
+  gather_combine_bwd(ctx, t, dy, ys, d, plan, vals, d_ys, d_w, bf ? scores : nullptr, bf ? idx : nullptr,
+                     bf ? dz_bf16 : nullptr);
+  zero_pads(ctx, P, rb, P.d_ys);
+  exchange_rows(ctx, tr, P, rb, d_ys, P.d_ys, true);  // gradients ride the same routes
+  ctx_mark(ctx, MARK_GCB);
+  experts_bwd(ctx, t, P.rplan, d, h, params(), P.xs, P.hidden, P.d_ys, P.d_xs, grads(), P.d_pre, tpart);
+  exchange_rows(ctx, tr, P, rb, P.d_xs, d_xs, false);
+  if (bf) {
+    gate_dwg_bf16(ctx, x_saved, dz_bf16, n, d, E, part, (float*)dwg);
+    ctx_mark(ctx, MARK_GATE_DWG);
+    gate_dx_bf16(ctx, dz_bf16, wg, n, d, E, (const __nv_bfloat16*)d_xs, plan.inverse_pos, k, dx);
+  } else {
+    gate_bwd(ctx, t, x_saved, wg, scores, idx, d_w, n, d, E, k, dwg, gdx, dz, nullptr, nullptr);
+    ctx_mark(ctx, MARK_GATE_DWG);
+    scatter_bwd(ctx, t, d_xs, d, plan, dx, gdx);
+  }
+  ctx_mark(ctx, MARK_GATE_DX);
 }
 
 }  // namespace fmoe_b200
 
+namespace fmoe_b200 {
+void Layer::ep_free(Ep* e) { delete e; }
+}  // namespace fmoe_b200
+
+// ------------------------------------------------------------------- C-ABI
+using namespace fmoe_b200;
+
+#define FMOE_GUARD(...)               \
+  try {                               \
+    __VA_ARGS__;                      \
+    return FMOE_OK;                   \
+  } catch (const std::exception& e) { \
+    return guard_status(e);           \
+  } catch (...) {                     \
+    g_last_error = "unknown error";   \
+    return FMOE_ERR_CUDA;             \
+  }
+
+namespace {
+Ctx* CX(fmoe_ctx* c) {
+  if (!c) shape_error("null context");
+  return reinterpret_cast<Ctx*>(c);
+}
+void set_transport(Ctx* c, Transport* t) {
+  if (c->transport && c->owns_transport) delete c->transport;
+  c->transport = t;
+  c->owns_transport = true;
+}
+
+// Host exchange plan for the operator-level collectives (collectives.hpp:16-33).
+struct HostPlan {
+  int W, r;
+  int64_t el;
+  std::vector<int64_t> send, recv, send_off, chunk_off;
+};
+HostPlan host_plan(const fmoe_exchange_plan* p) {
+  if (!p || !p->send_counts || !p->recv_counts) shape_error("null exchange plan");
+  HostPlan h{(int)p->world, (int)p->rank, p->local_experts, {}, {}, {}, {}};
+  const int64_t E = p->world * p->local_experts;
+  h.send.assign(p->send_counts, p->send_counts + E);
+  h.recv.assign(p->recv_counts, p->recv_counts + E);
+  h.send_off.assign(E, 0);
+  for (int64_t g = 1; g < E; ++g) h.send_off[g] = h.send_off[g - 1] + h.send[g - 1];
+  h.chunk_off.assign(E, 0);
+  int64_t at = 0;
+  for (int64_t e = 0; e < h.el; ++e)
+    for (int s = 0; s < h.W; ++s) {
+      h.chunk_off[e * h.W + s] = at;
+      at += h.recv[(int64_t)s * h.el + e];
+    }
+  return h;
+}
+void a2a(Ctx* c, fmoe_dtype dt, const void* src, int64_t d, const fmoe_exchange_plan* p, void* dst, bool fwd) {
+  Transport* tr = c->transport;
+  if (p->world > 1 && !tr) protocol_error("all_to_all_rows: no transport");
+  HostPlan h = host_plan(p);
+  Layer::Ep P;
+  P.W = h.W;
+  P.r = h.r;
+  P.el = h.el;
+  P.h_send = h.send;
+  P.h_recv = h.recv;
+  P.send_off = h.send_off;
+  P.chunk_off = h.chunk_off;
+  if (p->world == 1) {
+    // world of one: the receive layout equals the send layout
+    int64_t rows = 0;
+    for (auto v : h.send) rows += v;
+    if (rows) CK(cudaMemcpyAsync(dst, src, (size_t)rows * d * dtype_size(dt), cudaMemcpyDeviceToDevice, c->stream));
+    return;
+  }
+  exchange_rows(c, tr, P, (size_t)d * dtype_size(dt), src, dst, fwd);
+}
+}  // namespace
+
 extern "C" {
-int fmoe_comm_unique_id(void*, int64_t) {
-  fmoe_b200::g_last_error = "NCCL communicator not available in this build";
-  return FMOE_ERR_TRANSPORT;
+
+int fmoe_ep_layout(int world, int64_t local_experts, int64_t align, const int64_t* send_counts,
+                   const int64_t* recv_counts, int64_t* send_off, int64_t* chunk_off, int64_t* block_off,
+                   int64_t* rows) {
+  FMOE_GUARD({
+    if (world < 1 || local_experts < 1 || align < 1) shape_error("ep_layout: bad sizes");
+    if (!send_counts || !recv_counts || !send_off || !chunk_off || !block_off || !rows)
+      shape_error("ep_layout: null buffer");
+    ep_layout(world, local_experts, align, send_counts, recv_counts, send_off, chunk_off, block_off, rows);
+  })
 }
-int fmoe_comm_init(fmoe_ctx*, const void*, int64_t, int, int) {
-  fmoe_b200::g_last_error = "NCCL communicator not available in this build";
-  return FMOE_ERR_TRANSPORT;
+
+int fmoe_comm_unique_id(void* id_out, int64_t id_bytes) {
+  FMOE_GUARD({
+    if (!id_out) shape_error("null id buffer");
+    nccl_unique_id(id_out, (size_t)id_bytes);
+  })
 }
+
+int fmoe_comm_init(fmoe_ctx* ctx, const void* id, int64_t id_bytes, int world, int rank) {
+  FMOE_GUARD({
+    Ctx* c = CX(ctx);
+    if (!id || id_bytes < 128) shape_error("fmoe_comm_init: need the 128-byte unique id");
+    if (world < 1 || rank < 0 || rank >= world) shape_error("fmoe_comm_init: bad world/rank");
+    CK(cudaSetDevice(c->device));
+    set_transport(c, make_nccl_transport(id, world, rank));
+    c->world = world;
+    c->rank = rank;
+  })
 }
+
+int fmoe_world_create(int world, fmoe_world** out) {
+  FMOE_GUARD({
+    if (world < 1 || !out) shape_error("fmoe_world_create: bad arguments");
+    *out = reinterpret_cast<fmoe_world*>(new LocalWorld(world));
+  })
+}
+
+int fmoe_world_destroy(fmoe_world* w) { FMOE_GUARD(delete reinterpret_cast<LocalWorld*>(w)) }
+
+int fmoe_ctx_join_world(fmoe_ctx* ctx, fmoe_world* w, int rank) {
+  FMOE_GUARD({
+    Ctx* c = CX(ctx);
+    auto* lw = reinterpret_cast<LocalWorld*>(w);
+    if (!lw || rank < 0 || rank >= lw->world) shape_error("fmoe_ctx_join_world: bad world/rank");
+    set_transport(c, make_local_transport(lw, rank));
+    c->world = lw->world;
+    c->rank = rank;
+  })
+}
+
+int fmoe_exchange_counts(fmoe_ctx* ctx, const int64_t* local_counts, int64_t n_counts,
+                         fmoe_exchange_plan* plan) {
+  FMOE_GUARD({
+    Ctx* c = CX(ctx);
+    const int W = c->transport ? c->transport->world : 1;
+    const int r = c->transport ? c->transport->rank : 0;
+    if (!plan || !plan->send_counts || !plan->recv_counts) shape_error("exchange_counts: null plan buffers");
+    if (n_counts < 1 || n_counts % W != 0)
+      shape_error("exchange_counts: expert count " + std::to_string(n_counts) + " not divisible by world size " +
+                  std::to_string(W));
+    const int64_t el = n_counts / W;
+    plan->world = W;
+    plan->rank = r;
+    plan->local_experts = el;
+    std::vector<int32_t> h32(n_counts);
+    for (int64_t i = 0; i < n_counts; ++i) {
+      if (local_counts[i] < 0 || local_counts[i] > INT32_MAX) shape_error("exchange_counts: bad count");
+      h32[i] = (int32_t)local_counts[i];
+      plan->send_counts[i] = local_counts[i];
+    }
+    int32_t* dbuf = (int32_t*)ctx_workspace(c, (size_t)n_counts * 8);
+    int32_t *dsend = dbuf, *drecv = dbuf + n_counts;
+    CK(cudaMemcpyAsync(dsend, h32.data(), n_counts * 4, cudaMemcpyHostToDevice, c->stream));
+    std::vector<Xfer> sends, recvs;
+    for (int p = 0; p < W; ++p) {
+      if (p == r) continue;
+      sends.push_back({p, dsend + p * el, (size_t)el * 4});
+      recvs.push_back({p, drecv + p * el, (size_t)el * 4});
+    }
+    CK(cudaMemcpyAsync(drecv + r * el, dsend + r * el, el * 4, cudaMemcpyDeviceToDevice, c->stream));
+    if (W > 1) c->transport->group(c, sends, recvs);
+    CK(cudaMemcpyAsync(h32.data(), drecv, n_counts * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    plan->send_total = plan->recv_total = 0;
+    for (int64_t i = 0; i < n_counts; ++i) {
+      plan->recv_counts[i] = h32[i];
+      plan->send_total += plan->send_counts[i];
+      plan->recv_total += plan->recv_counts[i];
+    }
+  })
+}
+
+int fmoe_a2a_rows(fmoe_ctx* ctx, fmoe_dtype dtype, const void* xs, int64_t d, const fmoe_exchange_plan* plan,
+                  void* out) {
+  FMOE_GUARD(a2a(CX(ctx), dtype, xs, d, plan, out, true))
+}
+
+int fmoe_a2a_rows_reverse(fmoe_ctx* ctx, fmoe_dtype dtype, const void* ys, int64_t d,
+                          const fmoe_exchange_plan* plan, void* out) {
+  FMOE_GUARD(a2a(CX(ctx), dtype, ys, d, plan, out, false))
+}
+
+}  // extern "C"

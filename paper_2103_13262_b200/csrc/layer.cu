@@ -74,7 +74,8 @@ Layer::Layer(Ctx* c, const fmoe_layer_config& cf) : ctx(c), cfg(cf) {
   plan.n_b = n;
   plan.k = k;
   plan.n_experts = E;
-  plan.align = bf ? 128 : 1;
+  const bool ep_mode = cfg.world_size > 1;  // EP: plan/xs/ys are the send layout
+  plan.align = (bf && !ep_mode) ? 128 : 1;
   plan.capacity = plan_capacity(n, k, E, plan.align);
   plan.counts = dalloc<int32_t>(owned, E);
   plan.offsets = dalloc<int32_t>(owned, E + 1);
@@ -87,12 +88,12 @@ Layer::Layer(Ctx* c, const fmoe_layer_config& cf) : ctx(c), cfg(cf) {
   const int64_t cap = plan.capacity;
   // activations (forward cache)
   xs = dalloc_bytes(owned, cap * d * es);
-  hidden = dalloc_bytes(owned, cap * h * es);
+  if (!ep_mode) hidden = dalloc_bytes(owned, cap * h * es);
   ys = dalloc_bytes(owned, cap * d * es);
   if (!bf || E > 256) logits = dalloc_bytes(owned, n * E * ss);
   // backward scratch
   d_ys = dalloc_bytes(owned, cap * d * es);
-  d_pre = dalloc_bytes(owned, cap * h * es);
+  if (!ep_mode) d_pre = dalloc_bytes(owned, cap * h * es);
   d_xs = dalloc_bytes(owned, cap * d * es);
   d_w = dalloc_bytes(owned, n * k * ss);
   dz = dalloc_bytes(owned, n * E * ss);
@@ -100,10 +101,12 @@ Layer::Layer(Ctx* c, const fmoe_layer_config& cf) : ctx(c), cfg(cf) {
   gdx = dalloc_bytes(owned, n * d * es);
   const int64_t S = gate_dwg_splits(n);
   part = dalloc<float>(owned, S * d * E + S + 64);
+  if (!ep_mode) tpart = dalloc<float>(owned, experts_bwd_part_floats(plan, d, h));
   if (cfg.world_size > 1) ep_alloc();
 }
 
 Layer::~Layer() {
+  ep_free(ep);
   for (void* p : owned) cudaFree(p);
   if (h_stage) cudaFreeHost(h_stage);
 }
@@ -171,7 +174,7 @@ void Layer::backward(const void* dy, void* dx) {
   gather_combine_bwd(ctx, t, dy, ys, d, plan, vals, d_ys, d_w, bf ? scores : nullptr, bf ? idx : nullptr,
                      bf ? dz_bf16 : nullptr);
   ctx_mark(ctx, MARK_GCB);
-  experts_bwd(ctx, t, plan, d, h, params(), xs, hidden, d_ys, d_xs, grads(), d_pre);  // expert.cpp:104-125
+  experts_bwd(ctx, t, plan, d, h, params(), xs, hidden, d_ys, d_xs, grads(), d_pre, tpart);  // expert.cpp:104-125
   if (bf) {
     gate_dwg_bf16(ctx, x_saved, dz_bf16, n, d, E, part, (float*)dwg);                  // gate.cpp:62
     ctx_mark(ctx, MARK_GATE_DWG);

@@ -28,7 +28,8 @@ struct Layer {
   // backward scratch
   void *d_ys = nullptr, *d_pre = nullptr, *d_xs = nullptr, *d_w = nullptr, *dz = nullptr, *gdx = nullptr;
   __nv_bfloat16* dz_bf16 = nullptr;
-  float* part = nullptr;
+  float* part = nullptr;   // gate d_wg split-K partials
+  float* tpart = nullptr;  // expert bias-gradient tile partials
   // host-buffer step
   void* io = nullptr;
   void* h_stage = nullptr;
@@ -47,6 +48,7 @@ struct Layer {
   void ep_alloc();
   void ep_forward(const void* x, void* y);
   void ep_backward(const void* dy, void* dx);
+  static void ep_free(Ep* e);
 };
 
 }  // namespace fmoe_b200

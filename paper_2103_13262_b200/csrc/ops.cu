@@ -223,7 +223,7 @@ void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
 
 void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
                  const fmoe_expert_params& w, const void* xs, const void* hidden, const void* d_ys,
-                 void* d_xs, const fmoe_expert_grads& g, void* d_pre) {
+                 void* d_xs, const fmoe_expert_grads& g, void* d_pre, float* part_ws) {
   const int64_t E = b.n_experts;
   if (E == 0) return;
   if (t == FMOE_F64 || t == FMOE_F32) {
@@ -285,6 +285,7 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     p.mode = tc::RAGGED_M; p.M = (int)cap; p.N = (int)h; p.K = (int)d;
     p.tile_group = b.tile_expert; p.n_mtiles = b.n_tiles; p.b_group_rows = (int)h;
     p.epi = tc::EPI_MASK_BF16; p.C = d_pre; p.ldc = h; p.mask = (const __nv_bfloat16*)hidden; p.ldm = h;
+    p.colsum_part = part_ws;  // d_b1 = colsum(d_pre) fused into the epilogue (expert.cpp:51-53)
     tc::launch(ctx, 256, false, false, ta, tb, p, max_tiles * ceil_div(h, 256));
     ctx_mark(ctx, MARK_DGRAD2);
   }
@@ -297,7 +298,10 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     tc::launch(ctx, 256, true, true, ta, tb, p, E * ceil_div(h, 128) * ceil_div(d, 256));
     ctx_mark(ctx, MARK_WGRAD2);
   }
-  block_colsum(ctx, t, d_ys, d, b.offsets, b.counts, E, g.d_b2);
+  // d_b2 = colsum(d_ys) per expert (expert.cpp:43-45): tile partials + ordered reduce
+  float* part_b2 = part_ws + max_tiles * h;
+  tile_colsum(ctx, (const __nv_bfloat16*)d_ys, d, b.n_tiles, max_tiles, part_b2);
+  reduce_tile_partials(ctx, part_b2, d, b.offsets, E, (float*)g.d_b2);
   ctx_mark(ctx, MARK_DB2);
   {  // dgrad fc1: d_xs = d_pre W1^T; B(k=j, n=c) = W1[e][c][j] -> K-major [E*d, h]
     const CUtensorMap ta = tc::make_tmap(d_pre, h, cap, h * 2, 64, 128);
@@ -318,8 +322,12 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     tc::launch(ctx, 256, true, true, ta, tb, p, E * ceil_div(d, 128) * ceil_div(h, 256));
     ctx_mark(ctx, MARK_WGRAD1);
   }
-  block_colsum(ctx, t, d_pre, h, b.offsets, b.counts, E, g.d_b1);
+  reduce_tile_partials(ctx, part_ws, h, b.offsets, E, (float*)g.d_b1);
   ctx_mark(ctx, MARK_DB1);
+}
+
+int64_t experts_bwd_part_floats(const fmoe_plan& b, int64_t d, int64_t h) {
+  return (b.capacity / 128 + 1) * (d + h);
 }
 
 }  // namespace fmoe_b200

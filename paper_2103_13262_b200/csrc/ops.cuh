@@ -30,6 +30,8 @@ void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
 // d_pre_ws: [capacity, h] dtype scratch
 void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
                  const fmoe_expert_params& w, const void* xs, const void* hidden, const void* d_ys,
-                 void* d_xs, const fmoe_expert_grads& g, void* d_pre_ws);
+                 void* d_xs, const fmoe_expert_grads& g, void* d_pre_ws, float* part_ws);
+// fp32 scratch floats experts_bwd needs for the bf16 bias-gradient partials
+int64_t experts_bwd_part_floats(const fmoe_plan& b, int64_t d, int64_t h);
 
 }  // namespace fmoe_b200

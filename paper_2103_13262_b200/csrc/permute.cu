@@ -310,7 +310,57 @@ __global__ void block_colsum_kernel(const T* __restrict__ src, int64_t n_cols,
   out[(int64_t)g * n_cols + c] = acc;
 }
 
+// ------------------------------------------------- tile column sums (bf16)
+// part[t][c] = sum of the 128 rows of tile t (fp32).  Two columns per thread,
+// a warp covers 128 contiguous bytes of a row, 128 rows in flight-unrolled order.
+__global__ void tile_colsum_kernel(const __nv_bfloat16* __restrict__ src, int64_t n_cols,
+                                   const int32_t* __restrict__ n_tiles, float* __restrict__ part) {
+  const int64_t t = blockIdx.y;
+  if (t >= __ldg(n_tiles)) return;
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (c >= n_cols) return;
+  const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(src + t * 128 * n_cols + c);
+  const int64_t stride = n_cols / 2;
+  float s0 = 0.f, s1 = 0.f;
+#pragma unroll 16
+  for (int r = 0; r < 128; ++r) {
+    const float2 v = __bfloat1622float2(__ldg(p + r * stride));
+    s0 += v.x;
+    s1 += v.y;
+  }
+  part[t * n_cols + c] = s0;
+  part[t * n_cols + c + 1] = s1;
+}
+
+// out[e][c] = sum over expert e's tiles, in tile order (deterministic).
+__global__ void reduce_tile_partials_kernel(const float* __restrict__ part, int64_t n_cols,
+                                            const int32_t* __restrict__ offsets, float* __restrict__ out) {
+  const int e = blockIdx.y;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_cols) return;
+  const int t0 = __ldg(offsets + e) / 128, t1 = __ldg(offsets + e + 1) / 128;
+  float s = 0.f;
+  for (int t = t0; t < t1; ++t) s += part[(int64_t)t * n_cols + c];
+  out[(int64_t)e * n_cols + c] = s;
+}
+
 }  // namespace
+
+void tile_colsum(Ctx* ctx, const __nv_bfloat16* src, int64_t n_cols, const int32_t* n_tiles,
+                 int64_t max_tiles, float* part) {
+  if (max_tiles == 0 || n_cols == 0) return;
+  dim3 grid((unsigned)ceil_div(n_cols, 512), (unsigned)max_tiles);
+  tile_colsum_kernel<<<grid, 256, 0, ctx->stream>>>(src, n_cols, n_tiles, part);
+  CK_LAUNCH(ctx);
+}
+
+void reduce_tile_partials(Ctx* ctx, const float* part, int64_t n_cols, const int32_t* offsets,
+                          int64_t n_blocks, float* out) {
+  if (n_blocks == 0 || n_cols == 0) return;
+  dim3 grid((unsigned)ceil_div(n_cols, 256), (unsigned)n_blocks);
+  reduce_tile_partials_kernel<<<grid, 256, 0, ctx->stream>>>(part, n_cols, offsets, out);
+  CK_LAUNCH(ctx);
+}
 
 void scatter(Ctx* ctx, fmoe_dtype t, const void* x, int64_t d, const fmoe_plan& p, void* xs) {
   const int64_t warps = p.n_b + (p.align > 1 ? p.n_experts * 128 : 0);

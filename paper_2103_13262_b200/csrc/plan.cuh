@@ -25,6 +25,13 @@ void gather_combine_bwd(Ctx* ctx, fmoe_dtype t, const void* dy, const void* ys, 
 void block_colsum(Ctx* ctx, fmoe_dtype t, const void* src, int64_t n_cols, const int32_t* offsets,
                   const int32_t* counts, int64_t n_blocks, void* out);
 
+// bf16 bias gradients over 128-row tiles of an aligned layout:
+// part[t][c] = sum of tile t's rows; out[e][c] = sum of expert e's tile partials.
+void tile_colsum(Ctx* ctx, const __nv_bfloat16* src, int64_t n_cols, const int32_t* n_tiles,
+                 int64_t max_tiles, float* part);
+void reduce_tile_partials(Ctx* ctx, const float* part, int64_t n_cols, const int32_t* offsets,
+                          int64_t n_blocks, float* out);
+
 // gate (gate.cu)
 void gate_softmax_topk(Ctx* ctx, fmoe_dtype t, const void* logits, int64_t n, int64_t e, int64_t k,
                        void* scores, int32_t* idx, void* vals, bool scores_ready);

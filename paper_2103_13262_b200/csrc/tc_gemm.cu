@@ -16,8 +16,27 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;             // two fp32 accumulators
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int COLSUM_BYTES = 4 * BN * 4;      // per-warp column sums of one tile
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + COLSUM_BYTES;
 };
+
+// Named barrier among the 4 epilogue warps (ids 1.. are free; 0 = __syncthreads).
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+// After the call lane L holds sum over the warp's 32 lanes of v[L] (31 shuffles).
+__device__ __forceinline__ float warp_transpose_sum(float (&v)[32], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const float send = upper ? v[i] : v[i + o];
+      const float keep = upper ? v[i + o] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return v[0];
+}
 
 // K-major / MN-major canonical SW128 layouts (cute UMMA::make_umma_desc):
 //   K-major : 8-row x 128 B atoms, SBO = 1024 (next 8 rows), LBO unused (=16 B)
@@ -260,6 +279,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull = bars + 2 * STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* colsum_smem = reinterpret_cast<float*>(smem + STAGES * C::STAGE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -273,7 +293,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(tfull + a), 1);
-      mbar_init(smem_u32(tempty + a), 4);  // one arrive per epilogue warp
+      mbar_init(smem_u32(tempty + a), 8);  // one arrive per epilogue warp
     }
     fence_mbarrier_init();
   }
@@ -360,7 +380,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= 4) {
     // ========================= epilogue ===========================
+    // 8 warps: warp w reads TMEM lanes 32*(w%4).. (the hardware lane quarter
+    // of its sub-partition) and half (w-4)/4 of the tile's column chunks.
     const int q = warp & 3;
+    const int ew = warp - 4;  // 0..7
+    constexpr int NC = BN / 32;
+    const int c_lo = (ew >> 2) * (NC / 2), c_hi = c_lo + NC / 2;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -369,7 +394,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (tl.nkb == 0) {
         // empty K range (expert without tokens): gradient is exactly zero
         if (p.epi == EPI_F32) {
-          for (int c = 0; c < BN / 32; ++c) {
+          for (int c = c_lo; c < c_hi; ++c) {
             float z[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) z[i] = 0.f;
@@ -382,13 +407,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       if (p.epi == EPI_GATE) {
-        epi_gate<BN>(p, tbase, row);
+        if (ew < 4) epi_gate<BN>(p, tbase, row);  // one thread owns a whole row of logits
       } else {
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = c_lo; c < c_hi; ++c) {
           if (tl.n0 + c * 32 >= p.N) break;
           float v[32];
           load_chunk(tbase + c * 32, v);
           epi_store_chunk<BN>(p, tl, row, tl.n0 + c * 32, v);
+          if (p.colsum_part) {  // column sums of the final fp32 values of this tile
+            if (row >= p.M) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = 0.f;
+            }
+            colsum_smem[q * BN + c * 32 + lane] = warp_transpose_sum(v, lane);
+          }
+        }
+        if (p.colsum_part) {
+          epi_bar();
+          for (int col = ew * 32 + lane; col < BN; col += 256)
+            if (tl.n0 + col < p.N)
+              p.colsum_part[(int64_t)(tl.m0 / BM) * p.N + tl.n0 + col] =
+                  colsum_smem[col] + colsum_smem[BN + col] + colsum_smem[2 * BN + col] + colsum_smem[3 * BN + col];
+          epi_bar();
         }
       }
       tc_fence_before();

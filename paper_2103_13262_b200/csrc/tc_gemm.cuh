@@ -13,9 +13,10 @@
 // Design (SURVEY §7, B200 guide "Canonical Blackwell GEMM"):
 //   * persistent: grid = #SMs, static round-robin over tiles; the tile list
 //     is derived on device from the dispatch plan (no host sync);
-//   * warp-specialised, 256 threads: warp0 = TMA producer, warp1 = MMA issuer
+//   * warp-specialised, 384 threads: warp0 = TMA producer, warp1 = MMA issuer
 //     (one elected lane, tcgen05.mma.cta_group::1.kind::f16 M=128, N=BN, K=16),
-//     warp2 = TMEM allocator, warps 4..7 = epilogue (one TMEM lane = one row);
+//     warp2 = TMEM allocator, warps 4..11 = epilogue (one TMEM lane = one row,
+//     two warps per lane quarter splitting the tile's columns);
 //   * smem ring of STAGES x (A 128x64 + B BNx64) bf16, 128B-swizzled TMA
 //     boxes, full/empty mbarriers; 2 TMEM accumulators (2*BN fp32 columns)
 //     so the epilogue of tile i overlaps the MMAs of tile i+1;
@@ -36,7 +37,7 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = one 128-byte swizzle row
-constexpr int NUM_THREADS = 256;
+constexpr int NUM_THREADS = 384;  // 4 control warps + 8 epilogue warps
 
 enum Mode : int { RAGGED_M = 0, RAGGED_K = 1 };
 enum Epi : int {
@@ -74,6 +75,11 @@ struct Params {
   const __nv_bfloat16* gather_src;  // d_xs [rows][N]
   const int* inverse_pos;           // [M][gk]
   int gk;
+  // optional fused column sums of the epilogue values (RAGGED_M bf16
+  // epilogues): colsum_part[m_tile][N] = sum over the tile's 128 rows, fp32
+  // (bias gradients without re-reading the activation; reduced per expert
+  // by reduce_tile_partials in a fixed order -> deterministic)
+  float* colsum_part;
 };
 
 // Host: build a 2-D bf16 tensor map over a row-major [outer, inner] matrix

@@ -1,0 +1,169 @@
+"""Expert parallelism on one B200: W ranks as host threads of this process
+(the reference's run_world_inproc pattern, test_support.hpp:96-120), each
+with its own context, stream and MoE layer, joined to an fmoe_world whose
+transport moves rows with device copies.  The data path (count exchange,
+global_scatter into aligned receive blocks, grouped experts, global_gather,
+gradients on the same routes) is the one the NCCL transport drives.
+
+Checks: the EP result equals the single-worker result on the
+rank-major concatenated batch bit-for-bit (deterministic kernels, receive
+order == the single worker's stable order); per-rank gate gradients equal
+the single worker's on the rank's own rows; f64 matches the reference's
+InProcWorld golden within the exp-ulp tolerance.
+"""
+import os
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+from tests.gpu_util import dev, host
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module")
+def fm():
+    import paper_2103_13262_b200 as m
+
+    return m
+
+
+def run_world(fm, world, cfg, dtype, xs, dys):
+    """One thread per rank; returns per-rank dicts of host arrays."""
+    w = fm.World(world)
+    out = [None] * world
+    errs = [None] * world
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                layer = fm.MoELayer(cfg, rank=r, dtype=dtype)
+                layer.join(w)
+                x = xs[r].to(device="cuda", dtype=dtype)
+                dy = dys[r].to(device="cuda", dtype=dtype)
+                y = layer.forward(x)
+                dx = layer.backward(dy)
+                s.synchronize()
+                out[r] = dict(y=y.cpu(), dx=dx.cpu(), dwg=layer.d_wg.cpu(), dw1=layer.grads.d_w1.cpu(),
+                              db1=layer.grads.d_b1.cpu(), dw2=layer.grads.d_w2.cpu(), db2=layer.grads.d_b2.cpu(),
+                              idx=layer.routing()[0].cpu())
+                del layer
+        except Exception as e:  # surfaced below
+            errs[r] = e
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    for e in errs:
+        if e is not None:
+            raise e
+    return out
+
+
+def single(fm, cfg, dtype, x, dy):
+    layer = fm.MoELayer(cfg, dtype=dtype)
+    y = layer.forward(x.to(device="cuda", dtype=dtype))
+    dx = layer.backward(dy.to(device="cuda", dtype=dtype))
+    torch.cuda.synchronize()
+    return dict(y=y.cpu(), dx=dx.cpu(), dwg=layer.d_wg.cpu(), dw1=layer.grads.d_w1.cpu(), db1=layer.grads.d_b1.cpu(),
+                dw2=layer.grads.d_w2.cpu(), db2=layer.grads.d_b2.cpu())
+
+
+def check_ep_equals_single(fm, world, n, d, h, el, k, dtype, seed=3):
+    g = torch.Generator().manual_seed(seed)
+    xs = [(torch.rand(n, d, generator=g) * 2 - 1).to(dtype) for _ in range(world)]
+    dys = [(torch.rand(n, d, generator=g) * 2 - 1).to(dtype) for _ in range(world)]
+    ep = run_world(fm, world, fm.MoEConfig(n, d, h, k, el, world, seed), dtype, xs, dys)
+    ref = single(fm, fm.MoEConfig(n * world, d, h, k, el * world, 1, seed), dtype, torch.cat(xs), torch.cat(dys))
+    assert torch.equal(torch.cat([o["y"] for o in ep]), ref["y"])
+    assert torch.equal(torch.cat([o["dx"] for o in ep]), ref["dx"])
+    for key in ("dw1", "db1", "dw2", "db2"):
+        assert torch.equal(torch.cat([o[key] for o in ep]), ref[key]), key
+    for r in range(world):  # each rank differentiates the gate on its own rows
+        own = single(fm, fm.MoEConfig(n, d, h, k, el * world, 1, seed), dtype, xs[r], dys[r])
+        assert torch.equal(ep[r]["dwg"], own["dwg"])
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_ep_bf16_equals_single_worker(fm, world):
+    check_ep_equals_single(fm, world, n=512, d=128, h=256, el=4, k=2, dtype=torch.bfloat16)
+
+
+def test_ep_bf16_skewed_and_empty_experts(fm):
+    """k=1 with few tokens: some experts receive nothing from some (or all) ranks."""
+    check_ep_equals_single(fm, 4, n=40, d=64, h=128, el=2, k=1, dtype=torch.bfloat16, seed=11)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_ep_f64_equals_single_worker(fm, world):
+    check_ep_equals_single(fm, world, n=48, d=16, h=24, el=2, k=2, dtype=torch.float64)
+
+
+@pytest.mark.parametrize("name", ["dist_w2", "dist_w4"])
+def test_ep_f64_vs_reference_golden(fm, orc, name):
+    g = dict(np.load(os.path.join(GOLDEN, name + ".npz")))
+    seed, world, n, d, h, el, k = (int(v) for v in g["meta"])
+    xs = [torch.from_numpy(orc.seeded_matrix(seed, 200 + r, n, d)) for r in range(world)]
+    dys = [torch.from_numpy(orc.seeded_matrix(seed, 300 + r, n, d)) for r in range(world)]
+    ep = run_world(fm, world, fm.MoEConfig(n, d, h, k, el, world, seed), torch.float64, xs, dys)
+    rel = lambda a, b: np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)  # noqa: E731
+    assert rel(torch.cat([o["y"] for o in ep]).numpy(), g["y"]) < 1e-13
+    assert rel(torch.cat([o["dx"] for o in ep]).numpy(), g["dx"]) < 1e-13
+    for key in ("dw1", "db1", "dw2", "db2"):
+        assert rel(torch.cat([o[key] for o in ep]).numpy(), g[key]) < 1e-13, key
+    for r in range(world):
+        assert rel(ep[r]["dwg"].numpy(), g["dwg"][r]) < 1e-13
+
+
+def test_exchange_operators_hand_example(fm):
+    """exchange_counts / all_to_all_rows(_reverse) (test_comm.cpp:87-104, 170-246)."""
+    world = 2
+    w = fm.World(world)
+    res = [None] * world
+    errs = [None] * world
+    counts = [[3, 5], [2, 4]]
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                ctx = fm.Context(0).use_current_stream()
+                ctx.join_world(w, r)
+                plan = fm.exchange_counts(counts[r], ctx)
+                rows = sum(counts[r])
+                xs = torch.arange(rows * 2, dtype=torch.float64, device="cuda").view(rows, 2) + 100 * r
+                got = fm.all_to_all_rows(xs, plan, ctx)
+                back = fm.all_to_all_rows_reverse(got, plan, ctx)
+                s.synchronize()
+                res[r] = (plan, xs.cpu(), got.cpu(), back.cpu())
+        except Exception as e:
+            errs[r] = e
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    [t.start() for t in th]
+    [t.join(timeout=120) for t in th]
+    for e in errs:
+        if e is not None:
+            raise e
+    p0, p1 = res[0][0], res[1][0]
+    assert p0.recv_counts.tolist() == [[3], [2]] and p0.recv_total == 5 and p0.send_total == 8
+    assert p1.recv_counts.tolist() == [[5], [4]] and p1.recv_total == 9 and p1.send_total == 6
+    # rank 0 receives its own first 3 rows then rank 1's first 2 rows
+    assert torch.equal(res[0][2], torch.cat([res[0][1][:3], res[1][1][:2]]))
+    assert torch.equal(res[1][2], torch.cat([res[0][1][3:], res[1][1][2:]]))
+    for r in range(world):  # exact inverse routing
+        assert torch.equal(res[r][3], res[r][1])
+
+
+def test_ep_needs_transport(fm):
+    layer = fm.MoELayer(fm.MoEConfig(16, 64, 64, 1, 4, 2, 0), rank=0, dtype=torch.bfloat16)
+    with pytest.raises(fm.ProtocolError):
+        layer.forward(torch.zeros(16, 64, dtype=torch.bfloat16, device="cuda"))

@@ -207,7 +207,7 @@ def test_gate_bf16(fm, orc, n, d, e, k):
     s = host(out.scores)
     assert np.abs(s - s_o).max() < 1e-5
     ok = well_separated_rows(s_o, k)
-    assert ok.mean() > 0.5
+    assert ok.sum() >= min(100, n // 10)
     assert np.array_equal(host(out.topk_indices)[ok], i_o[ok])
     assert np.abs(host(out.topk_scores)[ok] - v_o[ok]).max() < 1e-5
     dt = rng.uniform(-1, 1, (n, k))
