@@ -51,7 +51,7 @@ void Layer::ep_alloc() {
   P.W = (int)cfg.world_size;
   P.r = (int)cfg.rank;
   P.el = cfg.n_e_local;
-  P.align = t == FMOE_BF16 ? 128 : 1;
+  P.align = t == FMOE_BF16 ? 256 : 1;  // CTA-pair GEMM tiles
   // worst case: every token of every rank picks this rank's experts
   P.cap_recv = plan_capacity(cfg.n_b * cfg.world_size, cfg.k, P.el, P.align);
   const int64_t d = cfg.d_m, h = cfg.d_h, cap = P.cap_recv;
@@ -204,7 +204,7 @@ static void ep_plan(Layer& L, Transport* tr) {
   for (int64_t e = 0; e <= el; ++e) uo[e] = (int32_t)P.block_off[e];
   int32_t* ut = uo + el + 1;
   int64_t nt = 0;
-  if (P.align == 128) {
+  if (P.align % 128 == 0) {
     for (int64_t e = 0; e < el; ++e)
       for (int64_t tt = P.block_off[e] / 128; tt < P.block_off[e + 1] / 128; ++tt) ut[nt++] = (int32_t)e;
   }
@@ -215,6 +215,8 @@ static void ep_plan(Layer& L, Transport* tr) {
   CK(cudaMemcpyAsync(P.rplan.n_tiles, ut + nt, 4, cudaMemcpyHostToDevice, ctx->stream));
   P.planned = true;
 }
+
+void Layer::ep_check() const { need_transport(ctx, cfg); }
 
 void Layer::ep_forward(const void* x, void* y) {
   Transport* tr = need_transport(ctx, cfg);

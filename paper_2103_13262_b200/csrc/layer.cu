@@ -75,7 +75,7 @@ Layer::Layer(Ctx* c, const fmoe_layer_config& cf) : ctx(c), cfg(cf) {
   plan.k = k;
   plan.n_experts = E;
   const bool ep_mode = cfg.world_size > 1;  // EP: plan/xs/ys are the send layout
-  plan.align = (bf && !ep_mode) ? 128 : 1;
+  plan.align = (bf && !ep_mode) ? 256 : 1;  // 256: CTA-pair GEMM tiles
   plan.capacity = plan_capacity(n, k, E, plan.align);
   plan.counts = dalloc<int32_t>(owned, E);
   plan.offsets = dalloc<int32_t>(owned, E + 1);
@@ -142,7 +142,10 @@ void Layer::init_weights() {
 
 void Layer::forward(const void* x, void* y) {
   const int64_t n = cfg.n_b, d = cfg.d_m, h = cfg.d_h, k = cfg.k;
+  // moe_layer.cpp:70-75: validate the transport before any work is issued
+  if (cfg.world_size > 1) ep_check();
   x_saved = x;
+  fwd_done = false;
   ctx_mark(ctx, MARK_FWD_BEGIN);
   gate_fwd(ctx, t, x, wg, n, d, E, k, scores, idx, vals, logits);  // gate.cpp:23-35
   ctx_mark(ctx, MARK_GATE);

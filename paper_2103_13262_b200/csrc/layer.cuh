@@ -46,6 +46,7 @@ struct Layer {
   void backward(const void* dy, void* dx);
   void step_host(const void* x_host, const void* dy_host, void* y_host, void* dx_host);
   void ep_alloc();
+  void ep_check() const;  // ProtocolError unless a matching transport is attached
   void ep_forward(const void* x, void* y);
   void ep_backward(const void* dy, void* dx);
   static void ep_free(Ep* e);

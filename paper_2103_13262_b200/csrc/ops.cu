@@ -35,6 +35,9 @@ void require_bf16_dims(int64_t d, int64_t h) {
                 std::to_string(d) + ", " + std::to_string(h) + ")");
 }
 
+// CTA-pair (cta_group::2) tiles need expert blocks aligned to 256 rows.
+int pair_mode(const fmoe_plan& b) { return b.align % 256 == 0 ? 2 : 1; }
+
 std::vector<int32_t> host_counts(Ctx* ctx, const fmoe_plan& b) {
   std::vector<int32_t> c((size_t)b.n_experts);
   if (!c.empty())
@@ -194,9 +197,10 @@ void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     return;
   }
   require_bf16_dims(d, h);
-  if (b.align != 128 || !b.tile_expert) shape_error("bf16 experts need a 128-aligned plan");
+  if (b.align % 128 != 0 || !b.tile_expert) shape_error("bf16 experts need a 128-row aligned plan");
+  const int cg = pair_mode(b);  // 256-aligned blocks -> CTA-pair tiles
   const int64_t cap = b.capacity;
-  const int64_t max_tiles = cap / 128;
+  const int64_t max_tiles = cap / (128 * cg);
   {  // fc1: A = xs [cap, d] K-major; B = W1 [E*d, h] MN-major
     const CUtensorMap ta = tc::make_tmap(xs, d, cap, d * 2, 64, 128);
     const CUtensorMap tb = tc::make_tmap(w.w1, h, E * d, h * 2, 64, 64);
@@ -205,7 +209,7 @@ void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     p.tile_group = b.tile_expert; p.n_mtiles = b.n_tiles; p.b_group_rows = (int)d;
     p.epi = tc::EPI_BF16; p.C = hidden; p.ldc = h;
     p.bias = (const float*)w.b1; p.bias_group_stride = h; p.relu = 1;
-    tc::launch(ctx, 256, false, true, ta, tb, p, max_tiles * ceil_div(h, 256));
+    tc::launch(ctx, 256, false, true, ta, tb, p, max_tiles * ceil_div(h, 256), cg);
     ctx_mark(ctx, MARK_FC1);
   }
   {  // fc2: A = hidden [cap, h] K-major; B = W2 [E*h, d] MN-major
@@ -216,7 +220,7 @@ void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     p.tile_group = b.tile_expert; p.n_mtiles = b.n_tiles; p.b_group_rows = (int)h;
     p.epi = tc::EPI_BF16; p.C = ys; p.ldc = d;
     p.bias = (const float*)w.b2; p.bias_group_stride = d; p.relu = 0;
-    tc::launch(ctx, 256, false, true, ta, tb, p, max_tiles * ceil_div(d, 256));
+    tc::launch(ctx, 256, false, true, ta, tb, p, max_tiles * ceil_div(d, 256), cg);
     ctx_mark(ctx, MARK_FC2);
   }
 }
@@ -275,18 +279,20 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     return;
   }
   require_bf16_dims(d, h);
-  if (b.align != 128 || !b.tile_expert) shape_error("bf16 experts need a 128-aligned plan");
+  if (b.align % 128 != 0 || !b.tile_expert) shape_error("bf16 experts need a 128-row aligned plan");
+  const int cg = pair_mode(b);
   const int64_t cap = b.capacity;
-  const int64_t max_tiles = cap / 128;
+  const int64_t max_tiles = cap / (128 * cg);  // (pair) row tiles
+  const int64_t t128 = cap / 128;              // 128-row tiles (bias partials)
   {  // dgrad fc2: d_pre = (d_ys W2^T) * (hidden > 0); B(k=c, n=j) = W2[e][j][c] -> K-major [E*h, d]
     const CUtensorMap ta = tc::make_tmap(d_ys, d, cap, d * 2, 64, 128);
-    const CUtensorMap tb = tc::make_tmap(w.w2, d, E * h, d * 2, 64, 256);
+    const CUtensorMap tb = tc::make_tmap(w.w2, d, E * h, d * 2, 64, 256 / cg);
     tc::Params p{};
     p.mode = tc::RAGGED_M; p.M = (int)cap; p.N = (int)h; p.K = (int)d;
     p.tile_group = b.tile_expert; p.n_mtiles = b.n_tiles; p.b_group_rows = (int)h;
     p.epi = tc::EPI_MASK_BF16; p.C = d_pre; p.ldc = h; p.mask = (const __nv_bfloat16*)hidden; p.ldm = h;
     p.colsum_part = part_ws;  // d_b1 = colsum(d_pre) fused into the epilogue (expert.cpp:51-53)
-    tc::launch(ctx, 256, false, false, ta, tb, p, max_tiles * ceil_div(h, 256));
+    tc::launch(ctx, 256, false, false, ta, tb, p, max_tiles * ceil_div(h, 256), cg);
     ctx_mark(ctx, MARK_DGRAD2);
   }
   {  // wgrad fc2: d_w2[e] = hidden_e^T d_ys_e  (M = h, N = d, K = rows of e)
@@ -295,22 +301,22 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     tc::Params p{};
     p.mode = tc::RAGGED_K; p.M = (int)h; p.N = (int)d; p.n_groups = (int)E; p.k_offsets = b.offsets;
     p.epi = tc::EPI_F32; p.C = g.d_w2; p.ldc = d; p.c_group_stride = h * d;
-    tc::launch(ctx, 256, true, true, ta, tb, p, E * ceil_div(h, 128) * ceil_div(d, 256));
+    tc::launch(ctx, 256, true, true, ta, tb, p, E * ceil_div(h, 128 * cg) * ceil_div(d, 256), cg);
     ctx_mark(ctx, MARK_WGRAD2);
   }
   // d_b2 = colsum(d_ys) per expert (expert.cpp:43-45): tile partials + ordered reduce
-  float* part_b2 = part_ws + max_tiles * h;
-  tile_colsum(ctx, (const __nv_bfloat16*)d_ys, d, b.n_tiles, max_tiles, part_b2);
+  float* part_b2 = part_ws + t128 * h;
+  tile_colsum(ctx, (const __nv_bfloat16*)d_ys, d, b.n_tiles, t128, part_b2);
   reduce_tile_partials(ctx, part_b2, d, b.offsets, E, (float*)g.d_b2);
   ctx_mark(ctx, MARK_DB2);
   {  // dgrad fc1: d_xs = d_pre W1^T; B(k=j, n=c) = W1[e][c][j] -> K-major [E*d, h]
     const CUtensorMap ta = tc::make_tmap(d_pre, h, cap, h * 2, 64, 128);
-    const CUtensorMap tb = tc::make_tmap(w.w1, h, E * d, h * 2, 64, 256);
+    const CUtensorMap tb = tc::make_tmap(w.w1, h, E * d, h * 2, 64, 256 / cg);
     tc::Params p{};
     p.mode = tc::RAGGED_M; p.M = (int)cap; p.N = (int)d; p.K = (int)h;
     p.tile_group = b.tile_expert; p.n_mtiles = b.n_tiles; p.b_group_rows = (int)d;
     p.epi = tc::EPI_BF16; p.C = d_xs; p.ldc = d;
-    tc::launch(ctx, 256, false, false, ta, tb, p, max_tiles * ceil_div(d, 256));
+    tc::launch(ctx, 256, false, false, ta, tb, p, max_tiles * ceil_div(d, 256), cg);
     ctx_mark(ctx, MARK_DGRAD1);
   }
   {  // wgrad fc1: d_w1[e] = xs_e^T d_pre_e  (M = d, N = h)
@@ -319,7 +325,7 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     tc::Params p{};
     p.mode = tc::RAGGED_K; p.M = (int)d; p.N = (int)h; p.n_groups = (int)E; p.k_offsets = b.offsets;
     p.epi = tc::EPI_F32; p.C = g.d_w1; p.ldc = h; p.c_group_stride = d * h;
-    tc::launch(ctx, 256, true, true, ta, tb, p, E * ceil_div(d, 128) * ceil_div(h, 256));
+    tc::launch(ctx, 256, true, true, ta, tb, p, E * ceil_div(d, 128 * cg) * ceil_div(h, 256), cg);
     ctx_mark(ctx, MARK_WGRAD1);
   }
   reduce_tile_partials(ctx, part_ws, h, b.offsets, E, (float*)g.d_b1);

@@ -49,9 +49,9 @@ __device__ __forceinline__ int64_t warp_id_global() {
   return ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
 }
 
-// Pad rows of an aligned plan: warp slot `w` -> (expert, r < 128).
+// Pad rows of an aligned plan: warp slot `w` -> (expert, r < align).
 __device__ __forceinline__ int64_t pad_row(const fmoe_plan& p, int64_t w) {
-  const int e = (int)(w >> 7), r = (int)(w & 127);
+  const int e = (int)(w / p.align), r = (int)(w % p.align);
   const int64_t row = (int64_t)p.offsets[e] + p.counts[e] + r;
   return row < p.offsets[e + 1] ? row : -1;
 }
@@ -363,7 +363,7 @@ void reduce_tile_partials(Ctx* ctx, const float* part, int64_t n_cols, const int
 }
 
 void scatter(Ctx* ctx, fmoe_dtype t, const void* x, int64_t d, const fmoe_plan& p, void* xs) {
-  const int64_t warps = p.n_b + (p.align > 1 ? p.n_experts * 128 : 0);
+  const int64_t warps = p.n_b + (p.align > 1 ? p.n_experts * p.align : 0);
   if (warps == 0) return;
   const unsigned grid = (unsigned)ceil_div(warps * 32, 256);
   scatter_kernel<<<grid, 256, 0, ctx->stream>>>(reinterpret_cast<const uint8_t*>(x),
@@ -401,7 +401,7 @@ void scatter_bwd(Ctx* ctx, fmoe_dtype t, const void* d_xs, int64_t d, const fmoe
 void gather_combine_bwd(Ctx* ctx, fmoe_dtype t, const void* dy, const void* ys, int64_t d,
                         const fmoe_plan& p, const void* w, void* d_ys, void* d_w,
                         const void* scores, const int32_t* topk_idx, __nv_bfloat16* dz) {
-  const int64_t warps = p.n_b + (p.align > 1 ? p.n_experts * 128 : 0);
+  const int64_t warps = p.n_b + (p.align > 1 ? p.n_experts * p.align : 0);
   if (warps == 0) return;
   if (dz && p.k > 8) shape_error("fused gate backward supports k <= 8");
   const unsigned grid = (unsigned)ceil_div(warps * 32, 256);

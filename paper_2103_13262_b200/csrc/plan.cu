@@ -186,7 +186,8 @@ void plan_build(Ctx* ctx, const int32_t* topk_idx, const fmoe_plan& p) {
   if (E < 1) shape_error("build_plan: need at least one expert");
   if ((int64_t)E * kWarpsPerCta * 4 > 200 * 1024)
     shape_error("build_plan: too many experts for the device plan (max 12800)");
-  if (p.align != 1 && p.align != 128) shape_error("build_plan: align must be 1 or 128");
+  if (p.align != 1 && p.align != 128 && p.align != 256)
+    shape_error("build_plan: align must be 1, 128 or 256");
   if (nk > (int64_t)1 << 30) shape_error("build_plan: n_b*k too large");
   const int64_t chunks = ceil_div(nk, kChunk);
   int32_t* chunk_hist = reinterpret_cast<int32_t*>(p.scratch);
@@ -205,7 +206,7 @@ void plan_build(Ctx* ctx, const int32_t* topk_idx, const fmoe_plan& p) {
   }
   plan_scan<<<1, 1024, (size_t)E * 4, ctx->stream>>>(chunk_hist, (int)chunks, E, (int)p.align,
                                                      p.capacity, p.counts, p.offsets, p.src_row,
-                                                     p.align == 128 ? p.tile_expert : nullptr,
+                                                     p.align % 128 == 0 ? p.tile_expert : nullptr,
                                                      p.n_tiles);
   CK_LAUNCH(ctx);
   if (nk > 0) {

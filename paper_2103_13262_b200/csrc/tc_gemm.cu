@@ -9,10 +9,12 @@
 namespace fmoe_b200 {
 namespace tc {
 
-template <int BN>
+// CG = CTAs per MMA (cta_group): 1 -> 128 x BN tiles per CTA; 2 -> 256 x BN tiles
+// per CTA pair, each CTA holding its 128 rows of A and BN/2 rows of B.
+template <int BN, int CG = 1>
 struct Cfg {
-  static constexpr int A_BYTES = BM * BK * 2;          // 16 KiB
-  static constexpr int B_BYTES = BN * BK * 2;          // 8/16/32 KiB
+  static constexpr int A_BYTES = BM * BK * 2;          // 16 KiB: this CTA's 128 rows
+  static constexpr int B_BYTES = (BN / CG) * BK * 2;   // this CTA's share of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;             // two fp32 accumulators
@@ -52,15 +54,15 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, bool mn) {
   return d;
 }
 
-// Instruction descriptor, kind::f16: D f32, A/B bf16, M=128, N=BN.
-template <int BN, bool A_MN, bool B_MN>
+// Instruction descriptor, kind::f16: D f32, A/B bf16, M=128*CG, N=BN.
+template <int BN, bool A_MN, bool B_MN, int CG>
 __device__ __forceinline__ constexpr uint32_t idesc() {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) | ((B_MN ? 1u : 0u) << 16) |
-         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((BM * CG) >> 4) << 24);
 }
 
 struct Tile {
-  int g, m0, n0, kbeg, nkb;
+  int g, m0, n0, kbeg, nkb;  // m0: first row of the (pair) tile
 };
 
 template <int BN>
@@ -68,34 +70,36 @@ __device__ __forceinline__ int n_tiles_n(const Params& p) {
   return (p.N + BN - 1) / BN;
 }
 
-template <int BN>
+// Tile rows = BM*CG.  RAGGED_M row tiles are counted in 128-row units by the
+// plan (n_mtiles, tile_group); with CG=2 the plan aligns expert blocks to 256.
+template <int BN, int CG>
 __device__ __forceinline__ int total_tiles(const Params& p) {
   const int nn = n_tiles_n<BN>(p);
   if (p.mode == RAGGED_M) {
-    const int nm = p.n_mtiles ? *p.n_mtiles : (p.M + BM - 1) / BM;
+    const int nm = p.n_mtiles ? (*p.n_mtiles + CG - 1) / CG : (p.M + BM * CG - 1) / (BM * CG);
     return nm * nn;
   }
-  return p.n_groups * ((p.M + BM - 1) / BM) * nn;
+  return p.n_groups * ((p.M + BM * CG - 1) / (BM * CG)) * nn;
 }
 
-template <int BN>
+template <int BN, int CG>
 __device__ __forceinline__ Tile decode(const Params& p, int t) {
   Tile r;
   const int nn = n_tiles_n<BN>(p);
   if (p.mode == RAGGED_M) {
     const int mt = t / nn;
     r.n0 = (t - mt * nn) * BN;
-    r.m0 = mt * BM;
-    r.g = p.tile_group ? __ldg(p.tile_group + mt) : 0;
+    r.m0 = mt * BM * CG;
+    r.g = p.tile_group ? __ldg(p.tile_group + mt * CG) : 0;
     r.kbeg = 0;
     r.nkb = (p.K + BK - 1) / BK;
   } else {
-    const int nm = (p.M + BM - 1) / BM;
+    const int nm = (p.M + BM * CG - 1) / (BM * CG);
     const int per = nm * nn;
     r.g = t / per;
     const int rem = t - r.g * per;
     const int mt = rem / nn;
-    r.m0 = mt * BM;
+    r.m0 = mt * BM * CG;
     r.n0 = (rem - mt * nn) * BN;
     r.kbeg = __ldg(p.k_offsets + r.g);
     const int kend = __ldg(p.k_offsets + r.g + 1);
@@ -263,12 +267,17 @@ __device__ __forceinline__ void epi_gate(const Params& p, uint32_t tbase, int ro
 }
 
 // ------------------------------------------------------------------ kernel
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const Params p) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, CG>;
   constexpr int STAGES = C::STAGES;
+  // CTA pair (CG=2): rank 0 (leader) issues the MMAs for both CTAs; both
+  // CTAs load their halves by TMA and drain their own TMEM rows.
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const int t0 = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int tstep = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -293,47 +302,63 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(tfull + a), 1);
-      mbar_init(smem_u32(tempty + a), 8);  // one arrive per epilogue warp
+      mbar_init(smem_u32(tempty + a), 8 * CG);  // one arrive per epilogue warp of the pair
     }
     fence_mbarrier_init();
   }
   if (warp == 2) {
-    tmem_alloc(smem_u32(tmem_slot), C::TMEM_COLS);
-    tmem_relinquish();
+    if (CG == 2) {
+      tmem_alloc_pair(smem_u32(tmem_slot), C::TMEM_COLS);
+      tmem_relinquish_pair();
+    } else {
+      tmem_alloc(smem_u32(tmem_slot), C::TMEM_COLS);
+      tmem_relinquish();
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync_all();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int total = total_tiles<BN>(p);
+  const int total = total_tiles<BN, CG>(p);
+  const int row_off = (int)rank * BM;             // this CTA's rows inside a pair tile
+  const int n_off = (int)rank * (BN / CG);        // this CTA's B rows (N) inside the tile
 
   if (warp == 0) {
     if (lane == 0) {
       // ======================= TMA producer =======================
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const Tile tl = decode<BN>(p, t);
+      for (int t = t0; t < total; t += tstep) {
+        const Tile tl = decode<BN, CG>(p, t);
         const int brow = (p.mode == RAGGED_M) ? tl.g * p.b_group_rows : tl.kbeg;
         for (int kb = 0; kb < tl.nkb; ++kb) {
           mbar_wait(smem_u32(empty + stage), phase ^ 1);
           const uint32_t fb = smem_u32(full + stage);
-          mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
+          if (rank == 0) mbar_arrive_expect_tx(fb, CG * C::STAGE_BYTES);
           const uint32_t a_dst = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_dst = smem_u32(sB + stage * C::B_BYTES);
+          auto load = [&](uint32_t dst, const CUtensorMap* m, int c0, int c1) {
+            if (CG == 2)
+              tma_load_2d_pair(dst, m, fb, c0, c1);
+            else
+              tma_load_2d(dst, m, fb, c0, c1);
+          };
           if (!A_MN) {
-            tma_load_2d(a_dst, &tmA, fb, kb * BK, tl.m0);
+            load(a_dst, &tmA, kb * BK, tl.m0 + row_off);
           } else {
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j)
-              tma_load_2d(a_dst + j * 8192, &tmA, fb, tl.m0 + 64 * j, tl.kbeg + kb * BK);
+              load(a_dst + j * 8192, &tmA, tl.m0 + row_off + 64 * j, tl.kbeg + kb * BK);
           }
           if (!B_MN) {
-            tma_load_2d(b_dst, &tmB, fb, kb * BK, brow + tl.n0);
+            load(b_dst, &tmB, kb * BK, brow + tl.n0 + n_off);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d(b_dst + j * 8192, &tmB, fb, tl.n0 + 64 * j, brow + kb * BK);
+            for (int j = 0; j < BN / CG / 64; ++j)
+              load(b_dst + j * 8192, &tmB, tl.n0 + n_off + 64 * j, brow + kb * BK);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -343,15 +368,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && rank == 0) {
       // ======================= MMA issuer =========================
-      constexpr uint32_t ID = idesc<BN, A_MN, B_MN>();
+      constexpr uint32_t ID = idesc<BN, A_MN, B_MN, CG>();
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const Tile tl = decode<BN>(p, t);
+      for (int t = t0; t < total; t += tstep) {
+        const Tile tl = decode<BN, CG>(p, t);
         if (tl.nkb == 0) continue;
         mbar_wait(smem_u32(tempty + acc), acc_phase ^ 1);
         tc_fence_after();
@@ -365,15 +390,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = sdesc(a_addr + (A_MN ? k * 2048 : k * 32), A_MN);
             const uint64_t bd = sdesc(b_addr + (B_MN ? k * 2048 : k * 32), B_MN);
-            tc_mma_f16(d_tmem, ad, bd, ID, (kb | k) != 0);
+            if (CG == 2)
+              tc_mma_f16_pair(d_tmem, ad, bd, ID, (kb | k) != 0);
+            else
+              tc_mma_f16(d_tmem, ad, bd, ID, (kb | k) != 0);
           }
-          tc_commit(smem_u32(empty + stage));
+          if (CG == 2)
+            tc_commit_pair(smem_u32(empty + stage));  // frees the stage in both CTAs
+          else
+            tc_commit(smem_u32(empty + stage));
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(smem_u32(tfull + acc));
+        if (CG == 2)
+          tc_commit_pair(smem_u32(tfull + acc));
+        else
+          tc_commit(smem_u32(tfull + acc));
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -388,9 +422,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int c_lo = (ew >> 2) * (NC / 2), c_hi = c_lo + NC / 2;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      const Tile tl = decode<BN>(p, t);
-      const int row = tl.m0 + q * 32 + lane;
+    for (int t = t0; t < total; t += tstep) {
+      const Tile tl = decode<BN, CG>(p, t);
+      const int row = tl.m0 + row_off + q * 32 + lane;
       if (tl.nkb == 0) {
         // empty K range (expert without tokens): gradient is exactly zero
         if (p.epi == EPI_F32) {
@@ -408,6 +442,48 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       if (p.epi == EPI_GATE) {
         if (ew < 4) epi_gate<BN>(p, tbase, row);  // one thread owns a whole row of logits
+      } else if (p.epi == EPI_GATE_DX && p.gk <= 2) {
+        // scatter_backward gather fused with the gate d_x: the row's k source
+        // positions are read once per tile and both source rows of a chunk are
+        // requested before the TMEM load, so each chunk costs one memory latency.
+        int pos0 = 0, pos1 = 0;
+        if (row < p.M) {
+          pos0 = __ldg(p.inverse_pos + (int64_t)row * p.gk);
+          pos1 = p.gk > 1 ? __ldg(p.inverse_pos + (int64_t)row * p.gk + 1) : pos0;
+        }
+        for (int c = c_lo; c < c_hi; ++c) {
+          const int c0 = tl.n0 + c * 32;
+          if (c0 >= p.N) break;
+          uint4 ga[4], gb[4];
+          if (row < p.M) {
+            const uint4* sa = reinterpret_cast<const uint4*>(p.gather_src + (int64_t)pos0 * p.N + c0);
+            const uint4* sb = reinterpret_cast<const uint4*>(p.gather_src + (int64_t)pos1 * p.N + c0);
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              ga[q4] = __ldg(sa + q4);
+              gb[q4] = p.gk > 1 ? __ldg(sb + q4) : make_uint4(0, 0, 0, 0);
+            }
+          }
+          float v[32];
+          load_chunk(tbase + c * 32, v);
+          if (row < p.M) {
+            uint4 o[4];
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              const __nv_bfloat16* a8 = reinterpret_cast<const __nv_bfloat16*>(&ga[q4]);
+              const __nv_bfloat16* b8 = reinterpret_cast<const __nv_bfloat16*>(&gb[q4]);
+              float s[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i)  // (d_xs[pos0] + d_xs[pos1]) + gate d_x, slot order
+                s[i] = (__bfloat162float(a8[i]) + __bfloat162float(b8[i])) + v[q4 * 8 + i];
+              o[q4] = make_uint4(pack_bf16(s[0], s[1]), pack_bf16(s[2], s[3]), pack_bf16(s[4], s[5]),
+                                 pack_bf16(s[6], s[7]));
+            }
+            uint4* out = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.C) + (int64_t)row * p.ldc + c0);
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) out[q4] = o[q4];
+          }
+        }
       } else {
         for (int c = c_lo; c < c_hi; ++c) {
           if (tl.n0 + c * 32 >= p.N) break;
@@ -426,23 +502,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           epi_bar();
           for (int col = ew * 32 + lane; col < BN; col += 256)
             if (tl.n0 + col < p.N)
-              p.colsum_part[(int64_t)(tl.m0 / BM) * p.N + tl.n0 + col] =
+              p.colsum_part[(int64_t)((tl.m0 + row_off) / BM) * p.N + tl.n0 + col] =
                   colsum_smem[col] + colsum_smem[BN + col] + colsum_smem[2 * BN + col] + colsum_smem[3 * BN + col];
           epi_bar();
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(tempty + acc));
+      if (lane == 0) {  // the leader's MMA waits for both CTAs' epilogues
+        if (rank == 0)
+          mbar_arrive(smem_u32(tempty + acc));
+        else
+          mbar_arrive_cluster(mapa_shared(smem_u32(tempty + acc), 0));
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync_all();
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, C::TMEM_COLS);
+    if (CG == 2)
+      tmem_dealloc_pair(tmem_base, C::TMEM_COLS);
+    else
+      tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
 }
 
@@ -484,39 +571,55 @@ CUtensorMap make_tmap(const void* base, uint64_t inner, uint64_t outer, uint64_t
   return m;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int CG>
 static void launch_t(Ctx* ctx, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
                      int64_t max_tiles) {
-  auto kern = tc_gemm_kernel<BN, A_MN, B_MN>;
-  static bool attr_set[8] = {};
-  const int dev = ctx->device & 7;
-  if (!attr_set[dev]) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
-    attr_set[dev] = true;
-  }
-  int64_t grid = ctx->num_sms;
-  if (max_tiles < grid) grid = max_tiles;
-  if (grid < 1) return;
-  kern<<<(unsigned)grid, NUM_THREADS, Cfg<BN>::SMEM, ctx->stream>>>(ta, tb, p);
+  auto kern = tc_gemm_kernel<BN, A_MN, B_MN, CG>;
+  using C = Cfg<BN, CG>;
+  static std::once_flag attr_once[8];
+  std::call_once(attr_once[ctx->device & 7], [&] {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    if (CG == 2) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+  });
+  // persistent grid: one CTA (CG=1) or CTA pair (CG=2) per tile slot, <= #SMs
+  int64_t grid = ctx->num_sms / CG * CG;
+  if (max_tiles * CG < grid) grid = max_tiles * CG;
+  if (grid < CG) return;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
   CK_LAUNCH(ctx);
 }
 
 void launch(Ctx* ctx, int bn, bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
-            const Params& p, int64_t max_tiles) {
-#define FMOE_TC_CASE(BN_, AM, BM_)                          \
-  if (bn == BN_ && a_mn == AM && b_mn == BM_) {             \
-    launch_t<BN_, AM, BM_>(ctx, ta, tb, p, max_tiles);      \
-    return;                                                 \
+            const Params& p, int64_t max_tiles, int cg) {
+#define FMOE_TC_CASE(BN_, AM, BM_, CG_)                        \
+  if (bn == BN_ && a_mn == AM && b_mn == BM_ && cg == CG_) {   \
+    launch_t<BN_, AM, BM_, CG_>(ctx, ta, tb, p, max_tiles);    \
+    return;                                                    \
   }
-  FMOE_TC_CASE(256, false, true)   // expert fc1/fc2 forward
-  FMOE_TC_CASE(256, false, false)  // dgrad, gate dx
-  FMOE_TC_CASE(256, true, true)    // weight gradients
-  FMOE_TC_CASE(128, false, true)
-  FMOE_TC_CASE(128, false, false)
-  FMOE_TC_CASE(128, true, true)
-  FMOE_TC_CASE(64, false, true)    // gate logits (E <= 64), gate dWg partials
-  FMOE_TC_CASE(64, false, false)
-  FMOE_TC_CASE(64, true, true)
+  FMOE_TC_CASE(256, false, true, 2)   // expert fc1/fc2 (CTA pairs, 256 x 256 tiles)
+  FMOE_TC_CASE(256, false, false, 2)  // expert dgrad
+  FMOE_TC_CASE(256, true, true, 2)    // expert weight gradients
+  FMOE_TC_CASE(256, false, true, 1)
+  FMOE_TC_CASE(256, false, false, 1)  // gate dx
+  FMOE_TC_CASE(256, true, true, 1)
+  FMOE_TC_CASE(128, false, true, 1)
+  FMOE_TC_CASE(128, false, false, 1)
+  FMOE_TC_CASE(128, true, true, 1)
+  FMOE_TC_CASE(64, false, true, 1)    // gate logits (E <= 64), gate dWg partials
+  FMOE_TC_CASE(64, false, false, 1)
+  FMOE_TC_CASE(64, true, true, 1)
 #undef FMOE_TC_CASE
   shape_error("tc gemm: unsupported tile configuration");
 }

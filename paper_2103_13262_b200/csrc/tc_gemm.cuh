@@ -87,9 +87,11 @@ struct Params {
 CUtensorMap make_tmap(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
                       uint32_t box_inner, uint32_t box_outer);
 
-// Host: launch.  a_mn / b_mn select MN-major operands; bn in {64,128,256}.
+// Host: launch.  a_mn / b_mn select MN-major operands; bn in {64,128,256};
+// cg = 2 runs CTA pairs (tcgen05 cta_group::2, 256-row tiles; RAGGED_M then
+// needs 256-row aligned expert blocks).  max_tiles counts (pair) tiles.
 void launch(Ctx* ctx, int bn, bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
-            const Params& p, int64_t max_tiles);
+            const Params& p, int64_t max_tiles, int cg = 1);
 
 }  // namespace tc
 }  // namespace fmoe_b200

@@ -58,19 +58,20 @@ def test_plan_hand_example(fm):
     assert host(p.inverse_pos).tolist() == [[2, 5], [0, 3], [4, 1]]
 
 
+@pytest.mark.parametrize("align", [128, 256])
 @pytest.mark.parametrize("n,k,e", [(777, 2, 16), (4096, 2, 64), (20000, 1, 256), (300, 2, 40)])
-def test_plan_aligned_layout(fm, orc, n, k, e):
-    """align=128: same stable order inside each block, blocks start on tiles."""
+def test_plan_aligned_layout(fm, orc, n, k, e, align):
+    """aligned plans: same stable order inside each block, blocks start on tiles."""
     rng = np.random.default_rng(5 + n)
     p_ = 1.0 / np.arange(1, e + 1)
     idx = np.stack([rng.choice(e, size=k, replace=False, p=p_ / p_.sum()) for _ in range(n)])
     want = orc.build_plan(idx, e)
-    p = fm.build_plan(dev(idx, torch.int32), e, align=128)
+    p = fm.build_plan(dev(idx, torch.int32), e, align=align)
     counts = host(p.counts).astype(np.int64)
     off = host(p.offsets).astype(np.int64)
     assert beq(counts, want["counts"])
-    assert (off % 128 == 0).all()
-    assert np.array_equal(np.diff(off), (counts + 127) // 128 * 128)
+    assert (off % align == 0).all()
+    assert np.array_equal(np.diff(off), (counts + align - 1) // align * align)
     inv = host(p.inverse_pos).astype(np.int64)
     e_of = idx
     assert np.array_equal(inv - off[e_of], want["inverse_pos"] - want["offsets"][e_of])
@@ -252,13 +253,15 @@ def test_experts_f64_bit_exact(fm, orc, n, k, e, d, h):
         assert beq(host(g.d_w2[gi]), go["dw2"]) and beq(host(g.d_b2[gi]), go["db2"])
 
 
-@pytest.mark.parametrize("n,k,e,d,h", [(512, 2, 8, 128, 256), (3000, 2, 16, 64, 192), (1500, 1, 8, 256, 512)])
-def test_experts_bf16_vs_torch_fp32(fm, orc, n, k, e, d, h):
+@pytest.mark.parametrize("align", [128, 256])  # 128: one-CTA tiles; 256: CTA-pair (cta_group::2) tiles
+@pytest.mark.parametrize("n,k,e,d,h", [(512, 2, 8, 128, 256), (3000, 2, 16, 64, 192), (1500, 1, 8, 256, 512),
+                                       (700, 2, 4, 320, 448)])
+def test_experts_bf16_vs_torch_fp32(fm, orc, n, k, e, d, h, align):
     """Grouped tcgen05 GEMM (fc1/fc2, dgrad, wgrad) vs a plain PyTorch fp32
     reference of the same op on the same bf16 values."""
     rng = np.random.default_rng(n + d)
     idx = _blocks(orc, rng, n, k, e)
-    p = fm.build_plan(dev(idx, torch.int32), e, align=128)
+    p = fm.build_plan(dev(idx, torch.int32), e, align=align)
     w1 = torch.randn(e, d, h, device="cuda").mul(0.05).bfloat16()
     w2 = torch.randn(e, h, d, device="cuda").mul(0.05).bfloat16()
     b1 = torch.randn(e, h, device="cuda").mul(0.1)
