@@ -134,7 +134,7 @@ def cpu_tokens_for(cores: int) -> int:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -206,6 +206,7 @@ def run_ours(args, world, rank, cfg):
             layer.forward(x, y)
             layer.backward(dy, dx)
 
+        clocks = Clocks(local)  # sampled from the warm-up (under load) through the timed region
         for _ in range(max(args.warmup, 3) if args.warmup >= 0 else 3):
             step()
         ctx = layer.ctx
@@ -213,7 +214,6 @@ def run_ours(args, world, rank, cfg):
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
-        clocks = Clocks(local)
         launches0 = ctx.launches
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)

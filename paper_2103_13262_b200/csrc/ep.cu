@@ -75,6 +75,7 @@ void Layer::ep_alloc() {
   P.d_pre = alloc(owned, cap * h * es);
   P.d_xs = alloc(owned, cap * d * es);
   tpart = (float*)alloc(owned, experts_bwd_part_floats(P.rplan, d, h) * 4);
+  if (t == FMOE_BF16) relu_bits = (uint32_t*)alloc(owned, cap * (h / 32) * 4);
 }
 
 namespace {
@@ -230,7 +231,7 @@ void Layer::ep_forward(const void* x, void* y) {
   zero_pads(ctx, P, rb, P.xs);
   exchange_rows(ctx, tr, P, rb, xs, P.xs, true);   // C2 global_scatter
   ctx_mark(ctx, MARK_SCATTER);
-  experts_fwd(ctx, t, P.rplan, d, h, params(), P.xs, P.hidden, P.ys);
+  experts_fwd(ctx, t, P.rplan, d, h, params(), P.xs, P.hidden, P.ys, relu_bits);
   exchange_rows(ctx, tr, P, rb, P.ys, ys, false);  // C3 global_gather
   gather_combine(ctx, t, ys, d, plan, vals, y);
   ctx_mark(ctx, MARK_GATHER);
@@ -249,7 +250,8 @@ void Layer::ep_backward(const void* dy, void* dx) {
   zero_pads(ctx, P, rb, P.d_ys);
   exchange_rows(ctx, tr, P, rb, d_ys, P.d_ys, true);  // gradients ride the same routes
   ctx_mark(ctx, MARK_GCB);
-  experts_bwd(ctx, t, P.rplan, d, h, params(), P.xs, P.hidden, P.d_ys, P.d_xs, grads(), P.d_pre, tpart);
+  experts_bwd(ctx, t, P.rplan, d, h, params(), P.xs, P.hidden, P.d_ys, P.d_xs, grads(), P.d_pre, tpart,
+              relu_bits);
   exchange_rows(ctx, tr, P, rb, P.d_xs, d_xs, false);
   if (bf) {
     gate_dwg_bf16(ctx, x_saved, dz_bf16, n, d, E, part, (float*)dwg);

@@ -102,6 +102,7 @@ Layer::Layer(Ctx* c, const fmoe_layer_config& cf) : ctx(c), cfg(cf) {
   const int64_t S = gate_dwg_splits(n);
   part = dalloc<float>(owned, S * d * E + S + 64);
   if (!ep_mode) tpart = dalloc<float>(owned, experts_bwd_part_floats(plan, d, h));
+  if (!ep_mode && bf) relu_bits = dalloc<uint32_t>(owned, cap * (h / 32));
   if (cfg.world_size > 1) ep_alloc();
 }
 
@@ -158,7 +159,7 @@ void Layer::forward(const void* x, void* y) {
   ctx_mark(ctx, MARK_PLAN);
   scatter(ctx, t, x, d, plan, xs);                                // dispatch.cpp:49-59
   ctx_mark(ctx, MARK_SCATTER);
-  experts_fwd(ctx, t, plan, d, h, params(), xs, hidden, ys);      // expert.cpp:85-102
+  experts_fwd(ctx, t, plan, d, h, params(), xs, hidden, ys, relu_bits);  // expert.cpp:85-102
   gather_combine(ctx, t, ys, d, plan, vals, y);                   // dispatch.cpp:61-78
   ctx_mark(ctx, MARK_GATHER);
   fwd_done = true;
@@ -177,7 +178,8 @@ void Layer::backward(const void* dy, void* dx) {
   gather_combine_bwd(ctx, t, dy, ys, d, plan, vals, d_ys, d_w, bf ? scores : nullptr, bf ? idx : nullptr,
                      bf ? dz_bf16 : nullptr);
   ctx_mark(ctx, MARK_GCB);
-  experts_bwd(ctx, t, plan, d, h, params(), xs, hidden, d_ys, d_xs, grads(), d_pre, tpart);  // expert.cpp:104-125
+  experts_bwd(ctx, t, plan, d, h, params(), xs, hidden, d_ys, d_xs, grads(), d_pre, tpart,
+              relu_bits);  // expert.cpp:104-125
   if (bf) {
     gate_dwg_bf16(ctx, x_saved, dz_bf16, n, d, E, part, (float*)dwg);                  // gate.cpp:62
     ctx_mark(ctx, MARK_GATE_DWG);

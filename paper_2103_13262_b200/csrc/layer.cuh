@@ -30,6 +30,7 @@ struct Layer {
   __nv_bfloat16* dz_bf16 = nullptr;
   float* part = nullptr;   // gate d_wg split-K partials
   float* tpart = nullptr;  // expert bias-gradient tile partials
+  uint32_t* relu_bits = nullptr;  // bf16: hidden > 0 bitmap (fc1 -> dgrad fc2)
   // host-buffer step
   void* io = nullptr;
   void* h_stage = nullptr;

@@ -167,7 +167,8 @@ void gate_bwd(Ctx* ctx, fmoe_dtype t, const void* x, const void* wg, const void*
 
 // ----------------------------------------------------------------- experts
 void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
-                 const fmoe_expert_params& w, const void* xs, void* hidden, void* ys) {
+                 const fmoe_expert_params& w, const void* xs, void* hidden, void* ys,
+                 uint32_t* relu_bits) {
   const int64_t E = b.n_experts;
   if (E == 0 || b.capacity == 0) return;
   if (t == FMOE_F64 || t == FMOE_F32) {
@@ -209,6 +210,7 @@ void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     p.tile_group = b.tile_expert; p.n_mtiles = b.n_tiles; p.b_group_rows = (int)d;
     p.epi = tc::EPI_BF16; p.C = hidden; p.ldc = h;
     p.bias = (const float*)w.b1; p.bias_group_stride = h; p.relu = 1;
+    p.relu_bits_out = relu_bits;
     tc::launch(ctx, 256, false, true, ta, tb, p, max_tiles * ceil_div(h, 256), cg);
     ctx_mark(ctx, MARK_FC1);
   }
@@ -227,7 +229,8 @@ void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
 
 void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
                  const fmoe_expert_params& w, const void* xs, const void* hidden, const void* d_ys,
-                 void* d_xs, const fmoe_expert_grads& g, void* d_pre, float* part_ws) {
+                 void* d_xs, const fmoe_expert_grads& g, void* d_pre, float* part_ws,
+                 const uint32_t* relu_bits) {
   const int64_t E = b.n_experts;
   if (E == 0) return;
   if (t == FMOE_F64 || t == FMOE_F32) {
@@ -292,6 +295,7 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     p.tile_group = b.tile_expert; p.n_mtiles = b.n_tiles; p.b_group_rows = (int)h;
     p.epi = tc::EPI_MASK_BF16; p.C = d_pre; p.ldc = h; p.mask = (const __nv_bfloat16*)hidden; p.ldm = h;
     p.colsum_part = part_ws;  // d_b1 = colsum(d_pre) fused into the epilogue (expert.cpp:51-53)
+    p.relu_bits = relu_bits;  // 1 bit per activation instead of re-reading hidden
     tc::launch(ctx, 256, false, false, ta, tb, p, max_tiles * ceil_div(h, 256), cg);
     ctx_mark(ctx, MARK_DGRAD2);
   }

@@ -25,12 +25,16 @@ int64_t gate_dwg_splits(int64_t n);
 void gate_dx_bf16(Ctx* ctx, const __nv_bfloat16* dz, const void* wg, int64_t n, int64_t d, int64_t e,
                   const __nv_bfloat16* d_xs, const int32_t* inverse_pos, int64_t k, void* d_x);
 
+// relu_bits (optional, bf16): [capacity, h/32] bitmap of hidden > 0 written by
+// fc1 and consumed by experts_bwd instead of re-reading `hidden` for the mask.
 void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
-                 const fmoe_expert_params& w, const void* xs, void* hidden, void* ys);
+                 const fmoe_expert_params& w, const void* xs, void* hidden, void* ys,
+                 uint32_t* relu_bits = nullptr);
 // d_pre_ws: [capacity, h] dtype scratch
 void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
                  const fmoe_expert_params& w, const void* xs, const void* hidden, const void* d_ys,
-                 void* d_xs, const fmoe_expert_grads& g, void* d_pre_ws, float* part_ws);
+                 void* d_xs, const fmoe_expert_grads& g, void* d_pre_ws, float* part_ws,
+                 const uint32_t* relu_bits = nullptr);
 // fp32 scratch floats experts_bwd needs for the bf16 bias-gradient partials
 int64_t experts_bwd_part_floats(const fmoe_plan& b, int64_t d, int64_t h);
 

@@ -114,11 +114,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int BN>
+template <int BN, int EPI>
 __device__ __forceinline__ void epi_store_chunk(const Params& p, const Tile& tl, int row, int c0,
-                                                float (&v)[32]) {
+                                                float (&v)[32], uint32_t bits = 0) {
   // row: absolute row in the output tile space; c0: absolute column of v[0]
-  if (p.epi == EPI_F32) {
+  if constexpr (EPI == EPI_F32) {
     float* out = reinterpret_cast<float*>(p.C) + (int64_t)tl.g * p.c_group_stride +
                  (int64_t)row * p.ldc + c0;
     if (row >= p.M) return;
@@ -134,7 +134,7 @@ __device__ __forceinline__ void epi_store_chunk(const Params& p, const Tile& tl,
   }
   // bf16 outputs (RAGGED_M row space)
   if (row >= p.M) return;
-  if (p.epi == EPI_BF16) {
+  if constexpr (EPI == EPI_BF16) {
     if (p.bias) {
       const float* b = p.bias + (int64_t)tl.g * p.bias_group_stride + c0;
 #pragma unroll
@@ -147,8 +147,18 @@ __device__ __forceinline__ void epi_store_chunk(const Params& p, const Tile& tl,
     if (p.relu) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = v[i] < 0.f ? 0.f : v[i];
+      if (p.relu_bits_out) {
+        uint32_t b = 0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) b |= (v[i] > 0.f ? 1u : 0u) << i;
+        p.relu_bits_out[(int64_t)row * (p.N >> 5) + (c0 >> 5)] = b;
+      }
     }
-  } else if (p.epi == EPI_MASK_BF16) {
+  } else if constexpr (EPI == EPI_MASK_BF16) {
+    if (p.relu_bits) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = ((bits >> i) & 1u) ? v[i] : 0.f;
+    } else {
     const uint4* m = reinterpret_cast<const uint4*>(p.mask + (int64_t)row * p.ldm + c0);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -157,7 +167,8 @@ __device__ __forceinline__ void epi_store_chunk(const Params& p, const Tile& tl,
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[q * 8 + i] = __bfloat162float(mb[i]) > 0.f ? v[q * 8 + i] : 0.f;
     }
-  } else if (p.epi == EPI_GATE_DX) {
+    }
+  } else if constexpr (EPI == EPI_GATE_DX) {
     float s[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) s[i] = 0.f;
@@ -267,7 +278,7 @@ __device__ __forceinline__ void epi_gate(const Params& p, uint32_t tbase, int ro
 }
 
 // ------------------------------------------------------------------ kernel
-template <int BN, bool A_MN, bool B_MN, int CG>
+template <int BN, bool A_MN, bool B_MN, int CG, int EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const Params p) {
@@ -427,12 +438,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int row = tl.m0 + row_off + q * 32 + lane;
       if (tl.nkb == 0) {
         // empty K range (expert without tokens): gradient is exactly zero
-        if (p.epi == EPI_F32) {
+        if constexpr (EPI == EPI_F32) {
           for (int c = c_lo; c < c_hi; ++c) {
             float z[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) z[i] = 0.f;
-            if (tl.n0 + c * 32 < p.N) epi_store_chunk<BN>(p, tl, row, tl.n0 + c * 32, z);
+            if (tl.n0 + c * 32 < p.N) epi_store_chunk<BN, EPI>(p, tl, row, tl.n0 + c * 32, z);
           }
         }
         continue;
@@ -440,9 +451,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(smem_u32(tfull + acc), acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-      if (p.epi == EPI_GATE) {
+      if constexpr (EPI == EPI_GATE) {
         if (ew < 4) epi_gate<BN>(p, tbase, row);  // one thread owns a whole row of logits
-      } else if (p.epi == EPI_GATE_DX && p.gk <= 2) {
+      } else if (EPI == EPI_GATE_DX && p.gk <= 2) {
         // scatter_backward gather fused with the gate d_x: the row's k source
         // positions are read once per tile and both source rows of a chunk are
         // requested before the TMEM load, so each chunk costs one memory latency.
@@ -485,17 +496,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       } else {
-        for (int c = c_lo; c < c_hi; ++c) {
-          if (tl.n0 + c * 32 >= p.N) break;
-          float v[32];
-          load_chunk(tbase + c * 32, v);
-          epi_store_chunk<BN>(p, tl, row, tl.n0 + c * 32, v);
-          if (p.colsum_part) {  // column sums of the final fp32 values of this tile
-            if (row >= p.M) {
+        // Software-pipelined drain: the TMEM load of chunk i+1 is in flight
+        // while chunk i is transformed and stored; relu bitmaps are fetched
+        // up front.
+        constexpr int CPW = NC / 2;
+        uint32_t mbits[CPW];
 #pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        for (int i = 0; i < CPW; ++i) {
+          const int c0 = tl.n0 + (c_lo + i) * 32;
+          mbits[i] = (p.relu_bits && row < p.M && c0 < p.N)
+                         ? __ldg(p.relu_bits + (int64_t)row * (p.N >> 5) + (c0 >> 5))
+                         : 0u;
+        }
+        uint32_t buf[2][32];
+        if (tl.n0 + c_lo * 32 < p.N) tmem_ld_issue(tbase + c_lo * 32, buf[0]);
+#pragma unroll
+        for (int i = 0; i < CPW; ++i) {
+          const int c = c_lo + i;
+          if (tl.n0 + c * 32 < p.N) {
+            tmem_ld_wait(buf[i & 1]);
+            if (i + 1 < CPW && tl.n0 + (c + 1) * 32 < p.N) tmem_ld_issue(tbase + (c + 1) * 32, buf[(i + 1) & 1]);
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(buf[i & 1][j]);
+            epi_store_chunk<BN, EPI>(p, tl, row, tl.n0 + c * 32, v, mbits[i]);
+            if (p.colsum_part) {  // column sums of the final fp32 values of this tile
+              if (row >= p.M) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = 0.f;
+              }
+              colsum_smem[q * BN + c * 32 + lane] = warp_transpose_sum(v, lane);
             }
-            colsum_smem[q * BN + c * 32 + lane] = warp_transpose_sum(v, lane);
           }
         }
         if (p.colsum_part) {
@@ -571,15 +602,14 @@ CUtensorMap make_tmap(const void* base, uint64_t inner, uint64_t outer, uint64_t
   return m;
 }
 
-template <int BN, bool A_MN, bool B_MN, int CG>
+template <int BN, bool A_MN, bool B_MN, int CG, int EPI>
 static void launch_t(Ctx* ctx, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
                      int64_t max_tiles) {
-  auto kern = tc_gemm_kernel<BN, A_MN, B_MN, CG>;
+  auto kern = tc_gemm_kernel<BN, A_MN, B_MN, CG, EPI>;
   using C = Cfg<BN, CG>;
   static std::once_flag attr_once[8];
   std::call_once(attr_once[ctx->device & 7], [&] {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    if (CG == 2) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
   });
   // persistent grid: one CTA (CG=1) or CTA pair (CG=2) per tile slot, <= #SMs
   int64_t grid = ctx->num_sms / CG * CG;
@@ -601,25 +631,33 @@ static void launch_t(Ctx* ctx, const CUtensorMap& ta, const CUtensorMap& tb, con
   CK_LAUNCH(ctx);
 }
 
+// Only the (tile, operand-major, CTA-group, epilogue) combinations the MoE layer uses
+// are instantiated; each kernel carries exactly one epilogue.
 void launch(Ctx* ctx, int bn, bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
             const Params& p, int64_t max_tiles, int cg) {
-#define FMOE_TC_CASE(BN_, AM, BM_, CG_)                        \
-  if (bn == BN_ && a_mn == AM && b_mn == BM_ && cg == CG_) {   \
-    launch_t<BN_, AM, BM_, CG_>(ctx, ta, tb, p, max_tiles);    \
-    return;                                                    \
+#define FMOE_TC_CASE(BN_, AM, BM_, CG_, EPI_)                                   \
+  if (bn == BN_ && a_mn == AM && b_mn == BM_ && cg == CG_ && p.epi == EPI_) {   \
+    launch_t<BN_, AM, BM_, CG_, EPI_>(ctx, ta, tb, p, max_tiles);               \
+    return;                                                                     \
   }
-  FMOE_TC_CASE(256, false, true, 2)   // expert fc1/fc2 (CTA pairs, 256 x 256 tiles)
-  FMOE_TC_CASE(256, false, false, 2)  // expert dgrad
-  FMOE_TC_CASE(256, true, true, 2)    // expert weight gradients
-  FMOE_TC_CASE(256, false, true, 1)
-  FMOE_TC_CASE(256, false, false, 1)  // gate dx
-  FMOE_TC_CASE(256, true, true, 1)
-  FMOE_TC_CASE(128, false, true, 1)
-  FMOE_TC_CASE(128, false, false, 1)
-  FMOE_TC_CASE(128, true, true, 1)
-  FMOE_TC_CASE(64, false, true, 1)    // gate logits (E <= 64), gate dWg partials
-  FMOE_TC_CASE(64, false, false, 1)
-  FMOE_TC_CASE(64, true, true, 1)
+  // expert pool, CTA pairs (256-row aligned plans)
+  FMOE_TC_CASE(256, false, true, 2, EPI_BF16)        // fc1 (+bias, relu, relu bitmap), fc2 (+bias)
+  FMOE_TC_CASE(256, false, false, 2, EPI_MASK_BF16)  // dgrad fc2 (+relu mask, d_b1 column sums)
+  FMOE_TC_CASE(256, false, false, 2, EPI_BF16)       // dgrad fc1
+  FMOE_TC_CASE(256, true, true, 2, EPI_F32)          // weight gradients
+  // expert pool, single CTAs (128-row aligned plans)
+  FMOE_TC_CASE(256, false, true, 1, EPI_BF16)
+  FMOE_TC_CASE(256, false, false, 1, EPI_MASK_BF16)
+  FMOE_TC_CASE(256, false, false, 1, EPI_BF16)
+  FMOE_TC_CASE(256, true, true, 1, EPI_F32)
+  // gate
+  FMOE_TC_CASE(64, false, true, 1, EPI_GATE)         // logits + softmax + top-k, E <= 64
+  FMOE_TC_CASE(128, false, true, 1, EPI_GATE)        // E <= 128
+  FMOE_TC_CASE(256, false, true, 1, EPI_GATE)        // E <= 256
+  FMOE_TC_CASE(256, false, true, 1, EPI_F32)         // logits only, E > 256
+  FMOE_TC_CASE(256, false, false, 1, EPI_GATE_DX)    // gate d_x + scatter_backward
+  FMOE_TC_CASE(64, true, true, 1, EPI_F32)           // gate d_wg split-K partials
+  FMOE_TC_CASE(128, true, true, 1, EPI_F32)
 #undef FMOE_TC_CASE
   shape_error("tc gemm: unsupported tile configuration");
 }

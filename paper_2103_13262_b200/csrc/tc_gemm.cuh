@@ -80,6 +80,11 @@ struct Params {
   // (bias gradients without re-reading the activation; reduced per expert
   // by reduce_tile_partials in a fixed order -> deterministic)
   float* colsum_part;
+  // relu bitmaps [rows][N/32]: written by the fc1 epilogue (bit = value > 0),
+  // read by the dgrad-fc2 epilogue instead of the bf16 activations (64 MiB
+  // instead of 1 GiB at cfg2)
+  uint32_t* relu_bits_out;
+  const uint32_t* relu_bits;
 };
 
 // Host: build a 2-D bf16 tensor map over a row-major [outer, inner] matrix
