@@ -11,15 +11,20 @@ namespace tc {
 
 // CG = CTAs per MMA (cta_group): 1 -> 128 x BN tiles per CTA; 2 -> 256 x BN tiles
 // per CTA pair, each CTA holding its 128 rows of A and BN/2 rows of B.
-template <int BN, int CG = 1>
+template <int BN, int CG = 1, int EPI = EPI_F32>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;          // 16 KiB: this CTA's 128 rows
   static constexpr int B_BYTES = (BN / CG) * BK * 2;   // this CTA's share of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;             // two fp32 accumulators
   static constexpr int COLSUM_BYTES = 4 * BN * 4;      // per-warp column sums of one tile
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + COLSUM_BYTES;
+  // bf16 outputs leave through TMA stores: 8 epilogue warps x 2 buffers x
+  // (32 rows x 32 columns) staging tiles, 64B-swizzled
+  static constexpr bool TMA_STORE = EPI == EPI_BF16 || EPI == EPI_MASK_BF16;
+  static constexpr int STORE_BYTES = TMA_STORE ? 8 * 2 * 2048 : 0;
+  static constexpr int BUDGET = 200 * 1024 - STORE_BYTES - COLSUM_BYTES;
+  static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + STORE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + COLSUM_BYTES;
 };
 
 // Named barrier among the 4 epilogue warps (ids 1.. are free; 0 = __syncthreads).
@@ -114,9 +119,16 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Relu bitmap word of (row, 32-column chunk at c0), laid out so the 32 rows a
+// warp drains form one contiguous 128-byte line: [row/32][c0/32][row%32].
+__device__ __forceinline__ int64_t relu_bits_index(int row, int c0, int n) {
+  return (((int64_t)(row >> 5) * (n >> 5) + (c0 >> 5)) << 5) + (row & 31);
+}
+
 template <int BN, int EPI>
 __device__ __forceinline__ void epi_store_chunk(const Params& p, const Tile& tl, int row, int c0,
-                                                float (&v)[32], uint32_t bits = 0) {
+                                                float (&v)[32], uint32_t bits = 0,
+                                                uint32_t stage_addr = 0) {
   // row: absolute row in the output tile space; c0: absolute column of v[0]
   if constexpr (EPI == EPI_F32) {
     float* out = reinterpret_cast<float*>(p.C) + (int64_t)tl.g * p.c_group_stride +
@@ -132,9 +144,13 @@ __device__ __forceinline__ void epi_store_chunk(const Params& p, const Tile& tl,
     }
     return;
   }
-  // bf16 outputs (RAGGED_M row space)
-  if (row >= p.M) return;
-  if constexpr (EPI == EPI_BF16) {
+  // bf16 outputs (RAGGED_M row space).  With a TMA-store staging tile every
+  // lane still writes its (dummy) row; the tensor map clips rows >= M.
+  if (row >= p.M) {
+    if (!stage_addr) return;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = 0.f;
+  } else if constexpr (EPI == EPI_BF16) {
     if (p.bias) {
       const float* b = p.bias + (int64_t)tl.g * p.bias_group_stride + c0;
 #pragma unroll
@@ -151,7 +167,7 @@ __device__ __forceinline__ void epi_store_chunk(const Params& p, const Tile& tl,
         uint32_t b = 0;
 #pragma unroll
         for (int i = 0; i < 32; ++i) b |= (v[i] > 0.f ? 1u : 0u) << i;
-        p.relu_bits_out[(int64_t)row * (p.N >> 5) + (c0 >> 5)] = b;
+        p.relu_bits_out[relu_bits_index(row, c0, p.N)] = b;
       }
     }
   } else if constexpr (EPI == EPI_MASK_BF16) {
@@ -185,6 +201,21 @@ __device__ __forceinline__ void epi_store_chunk(const Params& p, const Tile& tl,
     }
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = s[i] + v[i];
+  }
+  if (stage_addr) {
+    // 32 rows x 64 B staging tile in the TMA SWIZZLE_64B layout: 16-byte chunk
+    // j of row r sits at r*64 + ((j ^ ((r >> 1) & 3)) << 4)
+    const uint32_t r = threadIdx.x & 31;
+    const uint32_t base = stage_addr + r * 64;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t a = base + (((uint32_t)q ^ ((r >> 1) & 3u)) << 4);
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+                   "r"(pack_bf16(v[q * 8 + 0], v[q * 8 + 1])), "r"(pack_bf16(v[q * 8 + 2], v[q * 8 + 3])),
+                   "r"(pack_bf16(v[q * 8 + 4], v[q * 8 + 5])), "r"(pack_bf16(v[q * 8 + 6], v[q * 8 + 7]))
+                   : "memory");
+    }
+    return;
   }
   __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.C) + (int64_t)row * p.ldc + c0;
   uint4* o4 = reinterpret_cast<uint4*>(out);
@@ -281,8 +312,8 @@ __device__ __forceinline__ void epi_gate(const Params& p, uint32_t tbase, int ro
 template <int BN, bool A_MN, bool B_MN, int CG, int EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const Params p) {
-  using C = Cfg<BN, CG>;
+                   const __grid_constant__ CUtensorMap tmC, const Params p) {
+  using C = Cfg<BN, CG, EPI>;
   constexpr int STAGES = C::STAGES;
   // CTA pair (CG=2): rank 0 (leader) issues the MMAs for both CTAs; both
   // CTAs load their halves by TMA and drain their own TMEM rows.
@@ -293,13 +324,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * C::A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
+  uint8_t* sOut = smem + STAGES * C::STAGE_BYTES;  // TMA-store staging (1024-aligned)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sOut + C::STORE_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
   uint64_t* tfull = bars + 2 * STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* colsum_smem = reinterpret_cast<float*>(smem + STAGES * C::STAGE_BYTES + 256);
+  float* colsum_smem = reinterpret_cast<float*>(sOut + C::STORE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -433,6 +465,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int c_lo = (ew >> 2) * (NC / 2), c_hi = c_lo + NC / 2;
     int acc = 0;
     uint32_t acc_phase = 0;
+    uint32_t sbuf = 0;  // TMA-store staging tile in use (per warp, double-buffered)
     for (int t = t0; t < total; t += tstep) {
       const Tile tl = decode<BN, CG>(p, t);
       const int row = tl.m0 + row_off + q * 32 + lane;
@@ -505,7 +538,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int i = 0; i < CPW; ++i) {
           const int c0 = tl.n0 + (c_lo + i) * 32;
           mbits[i] = (p.relu_bits && row < p.M && c0 < p.N)
-                         ? __ldg(p.relu_bits + (int64_t)row * (p.N >> 5) + (c0 >> 5))
+                         ? __ldg(p.relu_bits + relu_bits_index(row, c0, p.N))
                          : 0u;
         }
         uint32_t buf[2][32];
@@ -519,7 +552,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             float v[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(buf[i & 1][j]);
-            epi_store_chunk<BN, EPI>(p, tl, row, tl.n0 + c * 32, v, mbits[i]);
+            uint32_t stage = 0;
+            if constexpr (C::TMA_STORE) {  // reuse a staging tile only once its last TMA store read it
+              stage = smem_u32(sOut) + (uint32_t)((ew * 2 + sbuf) * 2048);
+              if (lane == 0) bulk_wait_read<1>();
+              __syncwarp();
+            }
+            epi_store_chunk<BN, EPI>(p, tl, row, tl.n0 + c * 32, v, mbits[i], stage);
+            if constexpr (C::TMA_STORE) {
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(&tmC, stage, tl.n0 + c * 32, tl.m0 + row_off + q * 32);
+                bulk_commit();
+              }
+              sbuf ^= 1;
+            }
             if (p.colsum_part) {  // column sums of the final fp32 values of this tile
               if (row >= p.M) {
 #pragma unroll
@@ -548,6 +596,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
+    }
+    if constexpr (C::TMA_STORE) {
+      if (lane == 0) bulk_wait_all();  // outputs written before the CTA retires
     }
   }
   tc_fence_before();
@@ -586,16 +637,18 @@ EncodeFn encode_fn() {
 }  // namespace
 
 CUtensorMap make_tmap(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
-                      uint32_t box_inner, uint32_t box_outer) {
+                      uint32_t box_inner, uint32_t box_outer, int swizzle) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {inner, outer};
   const cuuint64_t strides[1] = {row_bytes};
   const cuuint32_t box[2] = {box_inner, box_outer};
   const cuuint32_t es[2] = {1, 1};
+  const CUtensorMapSwizzle sw = swizzle == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                : CU_TENSOR_MAP_SWIZZLE_NONE;
   const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
-                                 strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                 strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw Error(FMOE_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) +
                                    ") inner=" + std::to_string(inner) + " outer=" + std::to_string(outer));
@@ -606,7 +659,11 @@ template <int BN, bool A_MN, bool B_MN, int CG, int EPI>
 static void launch_t(Ctx* ctx, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
                      int64_t max_tiles) {
   auto kern = tc_gemm_kernel<BN, A_MN, B_MN, CG, EPI>;
-  using C = Cfg<BN, CG>;
+  using C = Cfg<BN, CG, EPI>;
+  // bf16 outputs: [M rows][N cols] tensor map, 32x32 boxes matching the
+  // 64B-swizzled staging tiles of the epilogue warps
+  const CUtensorMap tc_out =
+      C::TMA_STORE ? make_tmap(p.C, p.N, p.M, p.ldc * 2, 32, 32, 64) : ta;
   static std::once_flag attr_once[8];
   std::call_once(attr_once[ctx->device & 7], [&] {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -627,7 +684,7 @@ static void launch_t(Ctx* ctx, const CUtensorMap& ta, const CUtensorMap& tb, con
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
+  CK(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc_out, p));
   CK_LAUNCH(ctx);
 }
 
