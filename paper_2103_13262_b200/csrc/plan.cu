@@ -4,10 +4,11 @@
 //
 //   K2a plan_hist  : one warp per chunk of 512 flat selections f = i*k + j;
 //                    __match_any_sync-aggregated shared-memory histogram
-//                    -> chunk_hist[c][e]; out-of-range index -> error flag.
-//   K2b plan_scan  : one CTA.  counts[e] = sum_c chunk_hist[c][e]; aligned
-//                    exclusive scan -> offsets; per-chunk bases
-//                    base[c][e] = offsets[e] + sum_{c'<c} hist[c'][e];
+//                    -> chunk_hist[e][c] (expert-major); out-of-range index
+//                    -> error flag.
+//   K2b plan_scan  : one CTA.  counts[e] = sum_c chunk_hist[e][c]; aligned
+//                    exclusive scan -> offsets; per-chunk bases (in place)
+//                    base[e][c] = offsets[e] + sum_{c'<c} hist[e][c'];
 //                    padding rows (src_row = -1); 128-row tile -> expert table.
 //   K2c plan_rank  : re-walks each chunk in order; within a 32-wide step the
 //                    rank of a lane among equal experts is popc(match & lt),
@@ -23,7 +24,9 @@ namespace fmoe_b200 {
 constexpr int kChunk = 512;       // selections per warp chunk
 constexpr int kWarpsPerCta = 4;
 
-__global__ void plan_hist(const int32_t* __restrict__ idx, int64_t nk, int n_experts,
+// chunk_hist is expert-major ([E][n_chunks]) so plan_scan reads each
+// expert's column contiguously.
+__global__ void plan_hist(const int32_t* __restrict__ idx, int64_t nk, int n_experts, int n_chunks,
                           int32_t* __restrict__ chunk_hist, int* __restrict__ err) {
   extern __shared__ int32_t sh[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -47,7 +50,7 @@ __global__ void plan_hist(const int32_t* __restrict__ idx, int64_t nk, int n_exp
       if (key >= 0 && (__ffs(peers) - 1) == lane) hist[key] += __popc(peers);
       __syncwarp();
     }
-    for (int e = lane; e < n_experts; e += 32) chunk_hist[chunk * n_experts + e] = hist[e];
+    for (int e = lane; e < n_experts; e += 32) chunk_hist[(int64_t)e * n_chunks + chunk] = hist[e];
   }
 }
 
@@ -72,7 +75,7 @@ __global__ void plan_scan(int32_t* __restrict__ chunk_hist, int n_chunks, int n_
   // phase 1: per-expert totals (one warp per expert column, lanes over chunks)
   for (int e = warp; e < n_experts; e += nwarps) {
     int s = 0;
-    for (int c = lane; c < n_chunks; c += 32) s += chunk_hist[(int64_t)c * n_experts + e];
+    for (int c = lane; c < n_chunks; c += 32) s += chunk_hist[(int64_t)e * n_chunks + c];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) {
@@ -113,18 +116,17 @@ __global__ void plan_scan(int32_t* __restrict__ chunk_hist, int n_chunks, int n_
     // lanes own contiguous chunk ranges so the scan follows chunk order
     const int cper = (n_chunks + 31) / 32;
     const int c0 = lane * cper, c1 = min(c0 + cper, n_chunks);
+    int32_t* col = chunk_hist + (int64_t)e * n_chunks;
     int loc = 0;
-    for (int c = c0; c < c1; ++c) loc += chunk_hist[(int64_t)c * n_experts + e];
+    for (int c = c0; c < c1; ++c) loc += col[c];
     const int ex = warp_incl_scan(loc, lane) - loc;
     int b = off + ex;
     for (int c = c0; c < c1; ++c) {
-      const int h = chunk_hist[(int64_t)c * n_experts + e];
-      chunk_hist[(int64_t)c * n_experts + e] = b;
+      const int h = col[c];
+      col[c] = b;
       b += h;
     }
     const int cnt = counts[e];
-    const int next = (e + 1 < n_experts) ? -1 : 0;  // resolved below
-    (void)next;
     const int end = off + (cnt + align - 1) / align * align;
     for (int r = off + cnt + lane; r < end; r += 32) src_row[r] = -1;
     if (tile_expert)
@@ -133,7 +135,7 @@ __global__ void plan_scan(int32_t* __restrict__ chunk_hist, int n_chunks, int n_
   (void)capacity;
 }
 
-__global__ void plan_rank(const int32_t* __restrict__ idx, int64_t nk, int k, int n_experts,
+__global__ void plan_rank(const int32_t* __restrict__ idx, int64_t nk, int k, int n_experts, int n_chunks,
                           const int32_t* __restrict__ chunk_base, int32_t* __restrict__ src_row,
                           int32_t* __restrict__ slot, int32_t* __restrict__ inverse_pos) {
   extern __shared__ int32_t sh[];
@@ -144,7 +146,7 @@ __global__ void plan_rank(const int32_t* __restrict__ idx, int64_t nk, int k, in
   const int64_t chunk = (int64_t)blockIdx.x * kWarpsPerCta + w;
   const int64_t f0 = chunk * kChunk;
   if (f0 >= nk) return;
-  const int32_t* base = chunk_base + chunk * n_experts;
+  const int32_t* base = chunk_base + chunk;  // base[key * n_chunks]
   const unsigned lt = (1u << lane) - 1u;
   for (int s = 0; s < kChunk; s += 32) {
     const int64_t f = f0 + s + lane;
@@ -158,7 +160,7 @@ __global__ void plan_rank(const int32_t* __restrict__ idx, int64_t nk, int k, in
     if (key >= 0) before = run[key];
     __syncwarp();
     if (key >= 0) {
-      const int pos = __ldg(base + key) + before + __popc(peers & lt);
+      const int pos = __ldg(base + (int64_t)key * n_chunks) + before + __popc(peers & lt);
       const int i = (int)(f / k);
       src_row[pos] = i;
       slot[pos] = (int)(f - (int64_t)i * k);
@@ -201,7 +203,8 @@ void plan_build(Ctx* ctx, const int32_t* topk_idx, const fmoe_plan& p) {
   }
   const unsigned grid = (unsigned)std::max<int64_t>(1, ceil_div(chunks, kWarpsPerCta));
   if (nk > 0) {
-    plan_hist<<<grid, 32 * kWarpsPerCta, smem, ctx->stream>>>(topk_idx, nk, E, chunk_hist, ctx->d_error);
+    plan_hist<<<grid, 32 * kWarpsPerCta, smem, ctx->stream>>>(topk_idx, nk, E, (int)chunks, chunk_hist,
+                                                              ctx->d_error);
     CK_LAUNCH(ctx);
   }
   plan_scan<<<1, 1024, (size_t)E * 4, ctx->stream>>>(chunk_hist, (int)chunks, E, (int)p.align,
@@ -210,7 +213,7 @@ void plan_build(Ctx* ctx, const int32_t* topk_idx, const fmoe_plan& p) {
                                                      p.n_tiles);
   CK_LAUNCH(ctx);
   if (nk > 0) {
-    plan_rank<<<grid, 32 * kWarpsPerCta, smem, ctx->stream>>>(topk_idx, nk, (int)p.k, E, chunk_hist,
+    plan_rank<<<grid, 32 * kWarpsPerCta, smem, ctx->stream>>>(topk_idx, nk, (int)p.k, E, (int)chunks, chunk_hist,
                                                               p.src_row, p.slot, p.inverse_pos);
     CK_LAUNCH(ctx);
   }

@@ -18,10 +18,14 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;             // two fp32 accumulators
   static constexpr int COLSUM_BYTES = 4 * BN * 4;      // per-warp column sums of one tile
-  // bf16 outputs leave through TMA stores: 8 epilogue warps x 2 buffers x
-  // (32 rows x 32 columns) staging tiles, 64B-swizzled
-  static constexpr bool TMA_STORE = EPI == EPI_BF16 || EPI == EPI_MASK_BF16;
-  static constexpr int STORE_BYTES = TMA_STORE ? 8 * 2 * 2048 : 0;
+  // outputs leave through TMA stores from (32 rows x 32 columns) staging
+  // tiles per epilogue warp: bf16 rows of 64 B (64B swizzle, double-buffered),
+  // fp32 rows of 128 B (128B swizzle, single buffer)
+  static constexpr bool TMA_STORE = EPI == EPI_BF16 || EPI == EPI_MASK_BF16 || EPI == EPI_F32;
+  static constexpr int OUT_ROW_BYTES = EPI == EPI_F32 ? 128 : 64;
+  static constexpr int NBUF = EPI == EPI_F32 ? 1 : 2;
+  static constexpr int TILE_BYTES = 32 * OUT_ROW_BYTES;
+  static constexpr int STORE_BYTES = TMA_STORE ? 8 * NBUF * TILE_BYTES : 0;
   static constexpr int BUDGET = 200 * 1024 - STORE_BYTES - COLSUM_BYTES;
   static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + STORE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + COLSUM_BYTES;
@@ -131,6 +135,23 @@ __device__ __forceinline__ void epi_store_chunk(const Params& p, const Tile& tl,
                                                 uint32_t stage_addr = 0) {
   // row: absolute row in the output tile space; c0: absolute column of v[0]
   if constexpr (EPI == EPI_F32) {
+    if (stage_addr) {
+      // 32 rows x 128 B staging tile, TMA SWIZZLE_128B layout: 16-byte chunk j
+      // of row r at r*128 + ((j ^ (r & 7)) << 4); rows >= M are clipped or
+      // never stored (tiles do not cross groups when TMA stores are enabled)
+      const uint32_t r = threadIdx.x & 31;
+      const uint32_t base = stage_addr + r * 128;
+      const bool live = row < p.M;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t a = base + (((uint32_t)j ^ (r & 7u)) << 4);
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(live ? v[4 * j] : 0.f),
+                     "f"(live ? v[4 * j + 1] : 0.f), "f"(live ? v[4 * j + 2] : 0.f),
+                     "f"(live ? v[4 * j + 3] : 0.f)
+                     : "memory");
+      }
+      return;
+    }
     float* out = reinterpret_cast<float*>(p.C) + (int64_t)tl.g * p.c_group_stride +
                  (int64_t)row * p.ldc + c0;
     if (row >= p.M) return;
@@ -553,20 +574,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(buf[i & 1][j]);
             uint32_t stage = 0;
-            if constexpr (C::TMA_STORE) {  // reuse a staging tile only once its last TMA store read it
-              stage = smem_u32(sOut) + (uint32_t)((ew * 2 + sbuf) * 2048);
-              if (lane == 0) bulk_wait_read<1>();
+            if (C::TMA_STORE && p.tma_out) {  // reuse a staging tile only once its last TMA store read it
+              stage = smem_u32(sOut) + (uint32_t)((ew * C::NBUF + sbuf) * C::TILE_BYTES);
+              if (lane == 0) bulk_wait_read<C::NBUF - 1>();
               __syncwarp();
             }
             epi_store_chunk<BN, EPI>(p, tl, row, tl.n0 + c * 32, v, mbits[i], stage);
-            if constexpr (C::TMA_STORE) {
+            if (C::TMA_STORE && p.tma_out) {
               fence_proxy_async_smem();
               __syncwarp();
               if (lane == 0) {
-                tma_store_2d(&tmC, stage, tl.n0 + c * 32, tl.m0 + row_off + q * 32);
+                // output row: group base (weight-gradient groups) + tile row + warp slab
+                const int out_row = (p.c_group_stride ? tl.g * (int)(p.c_group_stride / p.ldc) : 0) + tl.m0 +
+                                    row_off + q * 32;
+                tma_store_2d(&tmC, stage, tl.n0 + c * 32, out_row);
                 bulk_commit();
               }
-              sbuf ^= 1;
+              sbuf = (sbuf + 1) % C::NBUF;
             }
             if (p.colsum_part) {  // column sums of the final fp32 values of this tile
               if (row >= p.M) {
@@ -637,7 +661,7 @@ EncodeFn encode_fn() {
 }  // namespace
 
 CUtensorMap make_tmap(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
-                      uint32_t box_inner, uint32_t box_outer, int swizzle) {
+                      uint32_t box_inner, uint32_t box_outer, int swizzle, bool f32) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {inner, outer};
   const cuuint64_t strides[1] = {row_bytes};
@@ -646,7 +670,8 @@ CUtensorMap make_tmap(const void* base, uint64_t inner, uint64_t outer, uint64_t
   const CUtensorMapSwizzle sw = swizzle == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
                                 : swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                                                 : CU_TENSOR_MAP_SWIZZLE_NONE;
-  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+  const CUresult r = encode_fn()(&m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                                 2, const_cast<void*>(base), dims,
                                  strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
@@ -660,10 +685,27 @@ static void launch_t(Ctx* ctx, const CUtensorMap& ta, const CUtensorMap& tb, con
                      int64_t max_tiles) {
   auto kern = tc_gemm_kernel<BN, A_MN, B_MN, CG, EPI>;
   using C = Cfg<BN, CG, EPI>;
-  // bf16 outputs: [M rows][N cols] tensor map, 32x32 boxes matching the
-  // 64B-swizzled staging tiles of the epilogue warps
-  const CUtensorMap tc_out =
-      C::TMA_STORE ? make_tmap(p.C, p.N, p.M, p.ldc * 2, 32, 32, 64) : ta;
+  // Output tensor map for the TMA-store epilogue: 32x32 boxes matching the
+  // staging tiles (bf16: [M][N], 64B swizzle; fp32: [groups*M][N], 128B swizzle).
+  // fp32 group outputs use it only when no tile can cross into the next group.
+  Params q = p;
+  q.tma_out = 0;
+  CUtensorMap tc_out = ta;
+  if (C::TMA_STORE) {
+    if (EPI == EPI_F32) {
+      const bool grouped = p.c_group_stride != 0;
+      const bool ok = p.ldc == p.N && (p.N % 4) == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 &&
+                      (!grouped || (p.M % (BM * CG) == 0 && p.c_group_stride == (int64_t)p.M * p.ldc));
+      if (ok) {
+        const int64_t rows = grouped ? (int64_t)p.M * p.n_groups : p.M;
+        tc_out = make_tmap(p.C, p.N, rows, p.ldc * 4, 32, 32, 128, true);
+        q.tma_out = 1;
+      }
+    } else {
+      tc_out = make_tmap(p.C, p.N, p.M, p.ldc * 2, 32, 32, 64);
+      q.tma_out = 1;
+    }
+  }
   static std::once_flag attr_once[8];
   std::call_once(attr_once[ctx->device & 7], [&] {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -684,7 +726,7 @@ static void launch_t(Ctx* ctx, const CUtensorMap& ta, const CUtensorMap& tb, con
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc_out, p));
+  CK(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc_out, q));
   CK_LAUNCH(ctx);
 }
 

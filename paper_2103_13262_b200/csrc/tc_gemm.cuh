@@ -85,12 +85,13 @@ struct Params {
   // instead of 1 GiB at cfg2)
   uint32_t* relu_bits_out;
   const uint32_t* relu_bits;
+  int tma_out;  // set by launch(): outputs leave through TMA stores
 };
 
 // Host: build a 2-D bf16 tensor map over a row-major [outer, inner] matrix
 // with a (box_inner x box_outer) box, 128B swizzle, zero OOB fill.
 CUtensorMap make_tmap(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
-                      uint32_t box_inner, uint32_t box_outer, int swizzle = 128);
+                      uint32_t box_inner, uint32_t box_outer, int swizzle = 128, bool f32 = false);
 
 // Host: launch.  a_mn / b_mn select MN-major operands; bn in {64,128,256};
 // cg = 2 runs CTA pairs (tcgen05 cta_group::2, 256-row tiles; RAGGED_M then
