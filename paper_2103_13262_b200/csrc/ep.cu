@@ -256,7 +256,8 @@ void Layer::ep_backward(const void* dy, void* dx) {
   if (bf) {
     gate_dwg_bf16(ctx, x_saved, dz_bf16, n, d, E, part, (float*)dwg);
     ctx_mark(ctx, MARK_GATE_DWG);
-    gate_dx_bf16(ctx, dz_bf16, wg, n, d, E, (const __nv_bfloat16*)d_xs, plan.inverse_pos, k, dx);
+    gate_dx_bf16(ctx, dz_bf16, wg, n, d, E, nullptr, nullptr, 0, gdx);
+    scatter_bwd(ctx, t, d_xs, d, plan, dx, gdx);
   } else {
     gate_bwd(ctx, t, x_saved, wg, scores, idx, d_w, n, d, E, k, dwg, gdx, dz, nullptr, nullptr);
     ctx_mark(ctx, MARK_GATE_DWG);

@@ -183,7 +183,11 @@ void Layer::backward(const void* dy, void* dx) {
   if (bf) {
     gate_dwg_bf16(ctx, x_saved, dz_bf16, n, d, E, part, (float*)dwg);                  // gate.cpp:62
     ctx_mark(ctx, MARK_GATE_DWG);
-    gate_dx_bf16(ctx, dz_bf16, wg, n, d, E, (const __nv_bfloat16*)d_xs, plan.inverse_pos, k, dx);  // gate.cpp:63 + dispatch.cpp:80-95
+    // gate d_x on the tensor cores (gate.cpp:63, TMA-store epilogue), then
+    // scatter_backward adds it in the reference order (dispatch.cpp:80-95,
+    // moe_layer.cpp:140) as one HBM-bound pass
+    gate_dx_bf16(ctx, dz_bf16, wg, n, d, E, nullptr, nullptr, 0, gdx);
+    scatter_bwd(ctx, t, d_xs, d, plan, dx, gdx);
   } else {
     gate_bwd(ctx, t, x_saved, wg, scores, idx, d_w, n, d, E, k, dwg, gdx, dz, nullptr, nullptr);
     ctx_mark(ctx, MARK_GATE_DWG);

@@ -157,6 +157,7 @@ __global__ void scatter_bwd_kernel(const T* __restrict__ d_xs, int64_t d, fmoe_p
   const int k = (int)p.k;
   if ((d % V) == 0) {
     const int64_t nv = d / V;
+#pragma unroll 4
     for (int64_t c = lane; c < nv; c += 32) {
       A acc[V];
 #pragma unroll
