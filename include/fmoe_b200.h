@@ -3,8 +3,8 @@
  *
  * This is the drop-in boundary: plain pointers and sizes, no torch or C++
  * types.  Every entry point replaces one operator of the reference's C++ API
- * (/root/reference/proj/include/fmoe/*.hpp) and is cited below.  The C++
- * drop-in headers (include/fmoe/*.hpp, libfmoe_dropin.so) and the Python
+ * (reference: proj/include/fmoe/<name>.hpp) and is cited below.  The C++
+ * drop-in headers (include/fmoe/<name>.hpp, libfmoe_dropin.so) and the Python
  * package (paper_2103_13262_b200) are thin hosts over these symbols.
  *
  * Conventions
@@ -165,6 +165,34 @@ int fmoe_experts_bwd(fmoe_ctx* ctx, fmoe_dtype dtype, const fmoe_plan* blocks, i
                      int64_t d_h, fmoe_expert_params params, const void* xs, const void* hidden,
                      const void* d_ys, void* d_xs, fmoe_expert_grads grads);
 
+/* Expert operators with the reference's full ForwardCache (expert.hpp:31-35):
+ * preact = xs*w1 + b1 is kept next to hidden = relu(preact), and the backward
+ * masks with preact > 0 (relu_backward, matrix.cpp:147-153) exactly as
+ * expert_backward does (expert.cpp:47-48), so caches built by a host remain
+ * valid inputs.  FMOE_F64 / FMOE_F32 only. */
+int fmoe_experts_fwd_cached(fmoe_ctx* ctx, fmoe_dtype dtype, const fmoe_plan* blocks, int64_t d_m,
+                            int64_t d_h, fmoe_expert_params params, const void* xs, void* preact,
+                            void* hidden, void* ys);
+int fmoe_experts_bwd_cached(fmoe_ctx* ctx, fmoe_dtype dtype, const fmoe_plan* blocks, int64_t d_m,
+                            int64_t d_h, fmoe_expert_params params, const void* xs, const void* preact,
+                            const void* hidden, const void* d_ys, void* d_xs, fmoe_expert_grads grads);
+
+/* ------------------------------------------------ dense primitives (L0) */
+/* The matrix primitives the gate and experts are composed of, on the same
+ * kernels as the FMOE_F64 / FMOE_F32 operators, so compositions reproduce the
+ * operators' bits (test_gate.cpp:66-82).  FMOE_F64 / FMOE_F32 only.
+ * matmul (matrix.hpp:77; matrix.cpp:96-119): c[m,n] = a[m,p] * b[p,n], one
+ * fma chain per element over p ascending from +0.0. */
+int fmoe_matmul(fmoe_ctx* ctx, fmoe_dtype dtype, const void* a, const void* b, int64_t m, int64_t p,
+                int64_t n, void* c);
+/* softmax_rows (matrix.hpp:89; matrix.cpp:155-170). */
+int fmoe_softmax_rows(fmoe_ctx* ctx, fmoe_dtype dtype, const void* a, int64_t rows, int64_t cols,
+                      void* out);
+/* topk_rows (matrix.hpp:91-96; matrix.cpp:172-189): descending, ties -> lower
+ * column.  ShapeError when k is not in [1, cols]. */
+int fmoe_topk_rows(fmoe_ctx* ctx, fmoe_dtype dtype, const void* a, int64_t rows, int64_t cols,
+                   int64_t k, int32_t* idx, void* vals);
+
 /* --------------------------------------------------------- MoE layer (L3) */
 /* One rank's slice of the layer (moe_layer.hpp:17-38): config, replicated
  * gate, local experts g = rank*n_e_local + slot, device weights, gradients and
@@ -247,6 +275,15 @@ int fmoe_ep_layout(int world, int64_t local_experts, int64_t align, const int64_
 /* all_to_all_rows_reverse (collectives.hpp:48-50; collectives.cpp:205-265). */
 int fmoe_a2a_rows_reverse(fmoe_ctx* ctx, fmoe_dtype dtype, const void* ys, int64_t d,
                           const fmoe_exchange_plan* plan, void* out);
+
+/* allreduce_sum (collectives.hpp:52-53; collectives.cpp:266-292): in-place
+ * sum of n elements over the sorted rank list `group` (which must contain the
+ * calling rank), accumulated in ascending rank order so every member holds
+ * identical bytes.  ProtocolError for an empty/unsorted group, a caller
+ * outside it, or members contributing different element counts.  Every member
+ * of the world's transport must enter the call (SPMD).  FMOE_F64 / FMOE_F32. */
+int fmoe_allreduce_sum(fmoe_ctx* ctx, fmoe_dtype dtype, void* buf, int64_t n, const int* group,
+                       int64_t group_size);
 
 #ifdef __cplusplus
 }

@@ -35,5 +35,9 @@ from .api import (  # noqa: F401
     all_to_all_rows,
     all_to_all_rows_reverse,
     ep_layout,
+    allreduce_sum,
+    matmul,
+    softmax_rows,
+    topk_rows,
 )
 from ._lib import LIB_PATH  # noqa: F401

@@ -77,7 +77,8 @@ EXPORTS = [
     "fmoe_layer_routing", "fmoe_layer_fwd", "fmoe_layer_bwd", "fmoe_layer_step_host",
     "fmoe_comm_unique_id", "fmoe_comm_init", "fmoe_world_create", "fmoe_world_destroy",
     "fmoe_ctx_join_world", "fmoe_exchange_counts", "fmoe_ep_layout", "fmoe_a2a_rows",
-    "fmoe_a2a_rows_reverse",
+    "fmoe_a2a_rows_reverse", "fmoe_allreduce_sum", "fmoe_matmul", "fmoe_softmax_rows", "fmoe_topk_rows",
+    "fmoe_experts_fwd_cached", "fmoe_experts_bwd_cached",
 ]
 
 
@@ -132,6 +133,13 @@ def _load():
         "fmoe_layer_step_host": [vp, vp, vp, vp, vp],
         "fmoe_comm_unique_id": [vp, i64],
         "fmoe_comm_init": [vp, vp, i64, C.c_int, C.c_int],
+        "fmoe_allreduce_sum": [vp, C.c_int, vp, i64, vp, i64],
+        "fmoe_matmul": [vp, C.c_int, vp, vp, i64, i64, i64, vp],
+        "fmoe_softmax_rows": [vp, C.c_int, vp, i64, i64, vp],
+        "fmoe_topk_rows": [vp, C.c_int, vp, i64, i64, i64, vp, vp],
+        "fmoe_experts_fwd_cached": [vp, C.c_int, C.POINTER(Plan), i64, i64, ExpertParams, vp, vp, vp, vp],
+        "fmoe_experts_bwd_cached": [vp, C.c_int, C.POINTER(Plan), i64, i64, ExpertParams, vp, vp, vp, vp, vp,
+                                    ExpertGrads],
     }
     for name, args in sig.items():
         f = getattr(lib, name)

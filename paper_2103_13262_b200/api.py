@@ -171,6 +171,19 @@ def all_to_all_rows_reverse(ys: torch.Tensor, plan: ExchangePlan, ctx: Context) 
     return out
 
 
+def allreduce_sum(m: torch.Tensor, group, ctx: Context) -> torch.Tensor:
+    """allreduce_sum (collectives.hpp:52-53): sum over the sorted rank list
+    `group` in ascending rank order (identical bytes on every member).  Every
+    rank of ctx's world must enter the call.  fp64 / fp32."""
+    import numpy as np
+
+    m = _dev(m).contiguous()
+    out = m.clone()
+    g = np.ascontiguousarray(np.asarray(list(group), dtype=np.int32))
+    check(lib.fmoe_allreduce_sum(ctx.h, dtype_code(m.dtype), _p(out), out.numel(), g.ctypes.data, g.size))
+    return out
+
+
 def ep_layout(world: int, local_experts: int, align: int, send_counts, recv_counts):
     """Host layout of one exchange through the library (fmoe_ep_layout):
     (send_off [E], chunk_off [el, W], block_off [el+1], rows [el])."""
@@ -190,6 +203,44 @@ def ep_layout(world: int, local_experts: int, align: int, send_counts, recv_coun
 
 def _ctx(t: torch.Tensor) -> Context:
     return Context.get(t.device)
+
+
+# ---------------------------------------------------------- dense primitives
+def _simt(t: torch.Tensor, who: str) -> None:
+    if t.dtype not in (torch.float64, torch.float32):
+        raise ShapeError(f"{who}: fp64 or fp32 only")
+
+
+def matmul(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """matmul (matrix.hpp:77; matrix.cpp:96-119): one fma chain per element over
+    the inner index ascending from +0.0 -- the kernel the fp64/fp32 gate uses."""
+    a, b = _dev(a).contiguous(), _dev(b).contiguous()
+    _simt(a, "matmul")
+    if a.dim() != 2 or b.dim() != 2 or a.shape[1] != b.shape[0] or a.dtype != b.dtype:
+        raise ShapeError(f"matmul: shapes {tuple(a.shape)} x {tuple(b.shape)}")
+    c = torch.empty(a.shape[0], b.shape[1], dtype=a.dtype, device=a.device)
+    check(lib.fmoe_matmul(_ctx(a).h, dtype_code(a.dtype), _p(a), _p(b), a.shape[0], a.shape[1], b.shape[1], _p(c)))
+    return c
+
+
+def softmax_rows(a: torch.Tensor) -> torch.Tensor:
+    """softmax_rows (matrix.cpp:155-170), the gate's softmax."""
+    a = _dev(a).contiguous()
+    _simt(a, "softmax_rows")
+    out = torch.empty_like(a)
+    check(lib.fmoe_softmax_rows(_ctx(a).h, dtype_code(a.dtype), _p(a), a.shape[0], a.shape[1], _p(out)))
+    return out
+
+
+def topk_rows(a: torch.Tensor, k: int):
+    """topk_rows (matrix.cpp:172-189): (indices int32, values), largest first,
+    ties -> lower column."""
+    a = _dev(a).contiguous()
+    _simt(a, "topk_rows")
+    idx = torch.empty(a.shape[0], max(k, 0), dtype=torch.int32, device=a.device)
+    val = torch.empty(a.shape[0], max(k, 0), dtype=a.dtype, device=a.device)
+    check(lib.fmoe_topk_rows(_ctx(a).h, dtype_code(a.dtype), _p(a), a.shape[0], a.shape[1], k, _p(idx), _p(val)))
+    return idx, val
 
 
 # --------------------------------------------------------------------- gate

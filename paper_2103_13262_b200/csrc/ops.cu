@@ -27,6 +27,22 @@ __global__ void cast_f32_bf16(const float* __restrict__ in, __nv_bfloat16* __res
   if (i < n) out[i] = __float2bfloat16_rn(in[i]);
 }
 
+// relu (matrix.cpp:140-145): x < 0 -> 0, so -0.0 survives.
+template <typename T>
+__global__ void relu_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const T v = in[i];
+    out[i] = v < T(0) ? T(0) : v;
+  }
+}
+template <typename T>
+void relu_rows(Ctx* ctx, const T* in, T* out, int64_t n) {
+  if (n <= 0) return;
+  relu_kernel<T><<<(unsigned)ceil_div(n, 256), 256, 0, ctx->stream>>>(in, out, n);
+  CK_LAUNCH(ctx);
+}
+
 int pick_bn(int64_t n) { return n <= 64 ? 64 : n <= 128 ? 128 : 256; }
 
 void require_bf16_dims(int64_t d, int64_t h) {
@@ -168,7 +184,7 @@ void gate_bwd(Ctx* ctx, fmoe_dtype t, const void* x, const void* wg, const void*
 // ----------------------------------------------------------------- experts
 void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
                  const fmoe_expert_params& w, const void* xs, void* hidden, void* ys,
-                 uint32_t* relu_bits) {
+                 uint32_t* relu_bits, void* preact) {
   const int64_t E = b.n_experts;
   if (E == 0 || b.capacity == 0) return;
   if (t == FMOE_F64 || t == FMOE_F32) {
@@ -182,9 +198,10 @@ void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
       p.N = h; p.K = d;
       p.A = (const T*)xs; p.sa_m = d; p.sa_k = 1;
       p.B = (const T*)w.w1; p.sb_k = h; p.sb_n = 1; p.b_group_stride = d * h;
-      p.C = (T*)hidden; p.ldc = h;
-      p.bias = (const T*)w.b1; p.bias_group_stride = h; p.relu = 1;
+      p.C = (T*)(preact ? preact : hidden); p.ldc = h;
+      p.bias = (const T*)w.b1; p.bias_group_stride = h; p.relu = preact ? 0 : 1;
       simt_gemm<T>(ctx, p, max_m);
+      if (preact) relu_rows<T>(ctx, (const T*)preact, (T*)hidden, b.capacity * h);  // cache.preact kept
       SimtParams<T> q;  // ys = hidden W2 + b2       (expert.cpp:32)
       q.mode = SIMT_RAGGED_M; q.G = E; q.offsets = b.offsets; q.counts = b.counts;
       q.N = d; q.K = h;
@@ -230,7 +247,7 @@ void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
 void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
                  const fmoe_expert_params& w, const void* xs, const void* hidden, const void* d_ys,
                  void* d_xs, const fmoe_expert_grads& g, void* d_pre, float* part_ws,
-                 const uint32_t* relu_bits) {
+                 const uint32_t* relu_bits, const void* mask) {
   const int64_t E = b.n_experts;
   if (E == 0) return;
   if (t == FMOE_F64 || t == FMOE_F32) {
@@ -255,7 +272,7 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
         p.A = (const T*)d_ys; p.sa_m = d; p.sa_k = 1;
         p.B = (const T*)w.w2; p.sb_k = 1; p.sb_n = d; p.b_group_stride = h * d;
         p.C = (T*)d_pre; p.ldc = h;
-        p.mask = (const T*)hidden; p.ldm = h;
+        p.mask = (const T*)(mask ? mask : hidden); p.ldm = h;
         simt_gemm<T>(ctx, p, max_m);
       }
       {  // d_w1 = x^T d_pre (expert.cpp:50)

@@ -29,12 +29,15 @@ void gate_dx_bf16(Ctx* ctx, const __nv_bfloat16* dz, const void* wg, int64_t n, 
 // fc1 and consumed by experts_bwd instead of re-reading `hidden` for the mask.
 void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
                  const fmoe_expert_params& w, const void* xs, void* hidden, void* ys,
-                 uint32_t* relu_bits = nullptr);
-// d_pre_ws: [capacity, h] dtype scratch
+                 uint32_t* relu_bits = nullptr, void* preact = nullptr);
+// preact (SIMT dtypes only, optional): also keep x*w1 + b1 before the relu
+// (ForwardCache::preact, expert.hpp:31-35).
+// d_pre_ws: [capacity, h] dtype scratch; mask (SIMT dtypes only, optional): the
+// relu-backward operand, preact (strict > 0, matrix.cpp:147-153), default hidden.
 void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
                  const fmoe_expert_params& w, const void* xs, const void* hidden, const void* d_ys,
                  void* d_xs, const fmoe_expert_grads& g, void* d_pre_ws, float* part_ws,
-                 const uint32_t* relu_bits = nullptr);
+                 const uint32_t* relu_bits = nullptr, const void* mask = nullptr);
 // fp32 scratch floats experts_bwd needs for the bf16 bias-gradient partials
 int64_t experts_bwd_part_floats(const fmoe_plan& b, int64_t d, int64_t h);
 

@@ -1,0 +1,70 @@
+"""The reference's own C++ unit tests, compiled unchanged against the B200
+drop-in (include/fmoe/*.hpp + libfmoe_dropin.so over the C-ABI).
+
+tests/dropin/Makefile builds proj/tests/test_{tensor,gate,dispatch,expert,
+moe_layer}.cpp from the reference checkout with a minimal doctest stand-in
+(tests/dropin/doctest.h); the binaries travel to the GPU box with the
+snapshot.  Every operator they call runs on the GPU in the FMOE_F64 parity mode.
+
+Excluded test cases (out of the accelerated path):
+  * "checkpoint round trip" -- checkpoint files are not part of the drop-in.
+"""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "tests", "dropin", "_bin")
+LIB = os.path.join(ROOT, "paper_2103_13262_b200", "libfmoe_dropin.so")
+SUITES = ["test_tensor", "test_gate", "test_dispatch", "test_expert", "test_moe_layer"]
+EXCLUDE = {"test_moe_layer": ["checkpoint round trip"]}
+
+
+def test_dropin_library_exports_reference_api():
+    assert os.path.exists(LIB), "build() did not produce libfmoe_dropin.so"
+    syms = subprocess.run(["nm", "-DC", "--defined-only", LIB], capture_output=True, text=True, check=True).stdout
+    for name in ["fmoe::gate_forward(", "fmoe::gate_backward(", "fmoe::build_plan(", "fmoe::scatter(",
+                 "fmoe::gather_combine(", "fmoe::scatter_backward(", "fmoe::gather_combine_backward(",
+                 "fmoe::multi_expert_forward(", "fmoe::multi_expert_backward(", "fmoe::expert_forward(",
+                 "fmoe::expert_backward(", "fmoe::forward(", "fmoe::backward(", "fmoe::naive_forward(",
+                 "fmoe::init_state(", "fmoe::train_step(", "fmoe::exchange_counts(", "fmoe::all_to_all_rows(",
+                 "fmoe::all_to_all_rows_reverse(", "fmoe::allreduce_sum(", "fmoe::matmul(", "fmoe::softmax_rows(",
+                 "fmoe::topk_rows(", "fmoe::InProcWorld::transport("]:
+        assert name in syms, name
+    # the drop-in computes through the product library, never the checker
+    deps = subprocess.run(["ldd", LIB], capture_output=True, text=True).stdout
+    assert "libfmoe_b200.so" in deps and "orc" not in deps and "fmoe_ref" not in deps
+
+
+def _run(exe, exclude):
+    args = [exe] + (["--exclude=" + ",".join(exclude)] if exclude else [])
+    r = subprocess.run(args, capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    failed_cases = sorted(line.split("] ", 1)[1].split(" (")[0] for line in r.stdout.splitlines()
+                          if line.startswith("[ FAIL ]"))
+    failed_checks = sorted(line.split(": FAILED")[0].rsplit("/", 1)[-1] for line in out.splitlines()
+                           if ": FAILED" in line)
+    summary = [line for line in r.stdout.splitlines() if line.startswith("test cases:")]
+    return r.returncode, failed_cases, failed_checks, summary, out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("suite", SUITES)
+def test_reference_unit_tests_pass_on_dropin(suite):
+    """The drop-in passes exactly what the reference library passes on the same
+    test source: identical failing assertions (the reference itself fails
+    test_tensor.cpp:42,51,56 -- its naive loop is unfused, its matmul fused)."""
+    exe, ref = os.path.join(BIN, suite), os.path.join(BIN, "ref_" + suite)
+    if not os.path.exists(exe) or not os.path.exists(ref):
+        pytest.skip("reference unit tests were not compiled (build() needs the reference checkout)")
+    ex = EXCLUDE.get(suite, [])
+    rc, cases, checks, summary, out = _run(exe, ex)
+    rrc, rcases, rchecks, rsummary, rout = _run(ref, ex)
+    print("drop-in  :", summary, cases, checks)
+    print("reference:", rsummary, rcases, rchecks)
+    assert summary, out[-3000:]
+    assert (cases, checks) == (rcases, rchecks), out[-3000:]
+    assert rc == rrc
+    if suite != "test_tensor":
+        assert rc == 0 and "0 failed" in summary[0], out[-3000:]

@@ -167,3 +167,77 @@ def test_ep_needs_transport(fm):
     layer = fm.MoELayer(fm.MoEConfig(16, 64, 64, 1, 4, 2, 0), rank=0, dtype=torch.bfloat16)
     with pytest.raises(fm.ProtocolError):
         layer.forward(torch.zeros(16, 64, dtype=torch.bfloat16, device="cuda"))
+
+
+def _threads(fm, world, body):
+    w = fm.World(world)
+    res, errs = [None] * world, [None] * world
+
+    def run(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                ctx = fm.Context(0).use_current_stream()
+                ctx.join_world(w, r)
+                res[r] = body(r, ctx)
+                s.synchronize()
+        except Exception as e:  # noqa: BLE001
+            errs[r] = e
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    [t.start() for t in th]
+    [t.join(timeout=150) for t in th]
+    return res, errs
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_allreduce_sum_ascending_rank_order(fm, dtype):
+    """allreduce_sum (collectives.cpp:266-292; test_comm.cpp:256-292): the sum is
+    accumulated in ascending rank order and every member gets the same bytes."""
+    world = 4
+    g = torch.Generator().manual_seed(5)
+    ms = [torch.rand(7, 5, generator=g, dtype=torch.float64).to(dtype) * 10 ** r for r in range(world)]
+    groups = {0: [0, 1, 2, 3], 1: [0, 1, 2, 3], 2: [0, 1, 2, 3], 3: [0, 1, 2, 3]}
+
+    def body(r, ctx):
+        full = fm.allreduce_sum(ms[r].cuda(), groups[r], ctx).cpu()
+        # data-parallel style subgroups {0, 2} and {1, 3}
+        sub = fm.allreduce_sum(ms[r].cuda(), [r % 2, r % 2 + 2], ctx).cpu()
+        return full, sub
+
+    res, errs = _threads(fm, world, body)
+    for e in errs:
+        if e is not None:
+            raise e
+    want = ((ms[0] + ms[1]) + ms[2]) + ms[3]
+    for r in range(world):
+        assert torch.equal(res[r][0], want)
+        assert torch.equal(res[r][1], ms[r % 2] + ms[r % 2 + 2])
+
+
+def test_allreduce_sum_detects_shape_mismatch(fm):
+    """Ranks contributing different sizes raise ProtocolError on every member
+    (test_comm.cpp:294-316)."""
+    def body(r, ctx):
+        return fm.allreduce_sum(torch.ones(3 + r, dtype=torch.float64, device="cuda"), [0, 1], ctx)
+
+    res, errs = _threads(fm, 2, body)
+    assert all(isinstance(e, fm.ProtocolError) for e in errs), errs
+
+
+def test_allreduce_sum_rejects_bad_groups(fm):
+    def body(r, ctx):
+        out = []
+        for grp in ([], [1, 0], [1 - r]):
+            try:
+                fm.allreduce_sum(torch.ones(2, dtype=torch.float64, device="cuda"), grp, ctx)
+                out.append(None)
+            except fm.ProtocolError as e:
+                out.append(e)
+        return out
+
+    res, errs = _threads(fm, 2, body)
+    assert errs == [None, None]
+    for r in range(2):
+        assert all(isinstance(e, fm.ProtocolError) for e in res[r]), res[r]

@@ -385,3 +385,27 @@ def test_layer_shape_errors(fm):
     with pytest.raises(fm.ShapeError):
         fm.gate_forward(torch.zeros(4, 3, dtype=torch.float64, device="cuda"),
                         torch.zeros(4, 2, dtype=torch.float64, device="cuda"), 1)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_dense_primitives_compose_to_the_gate(fm, dtype):
+    """matmul -> softmax_rows -> topk_rows reproduce gate_forward bit for bit
+    (test_gate.cpp:66-82) and matmul is the reference's fma chain."""
+    g = torch.Generator().manual_seed(11)
+    x = (torch.rand(300, 70, generator=g, dtype=torch.float64) * 2 - 1).to(dtype).cuda()
+    w = (torch.rand(70, 24, generator=g, dtype=torch.float64) * 0.2 - 0.1).to(dtype).cuda()
+    out = fm.gate_forward(x, w, 3)
+    logits = fm.matmul(x, w)
+    s = fm.softmax_rows(logits)
+    idx, val = fm.topk_rows(s, 3)
+    assert torch.equal(out.scores, s)
+    assert torch.equal(out.topk_indices, idx)
+    assert torch.equal(out.topk_scores, val)
+    if dtype == torch.float64:  # the reference's fma chain (oracle matmul, matrix.cpp:56-88)
+        from oracle import orc
+
+        assert np.array_equal(logits.cpu().numpy(), orc.matmul(x.cpu().numpy(), w.cpu().numpy()))
+    with pytest.raises(fm.ShapeError):
+        fm.topk_rows(s, 25)
+    with pytest.raises(fm.ShapeError):
+        fm.matmul(x, x)
