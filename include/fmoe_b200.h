@@ -227,6 +227,19 @@ int fmoe_layer_bwd(fmoe_layer* layer, const void* dy, void* dx);
 int fmoe_layer_step_host(fmoe_layer* layer, const void* x_host, const void* dy_host,
                          void* y_host, void* dx_host);
 
+/* train_step (moe_layer.cpp:144-205) on device: forward, mean-squared error
+ * against target [n_b, d_m] (dtype) with d_y = 2*(y - target)/n, backward,
+ * under EP expert gradients * 1/W and the gate gradient averaged over the
+ * world (sync_gradients, param_sync.cpp:46-61, as fmoe_allreduce_sum), then
+ * SGD p -= lr*g on every parameter (sgd_step, param_sync.cpp:63-66).  *loss
+ * (may be NULL) receives the world-average loss; one host sync per call.
+ * FMOE_F64 reproduces the reference's arithmetic; FMOE_BF16 updates fp32
+ * master copies of the bf16 weights (widened from the bf16 values on the first
+ * step after fmoe_layer_init_weights or fmoe_layer_sync_masters -- call the
+ * latter after writing the weights through fmoe_layer_params). */
+int fmoe_layer_train_step(fmoe_layer* layer, const void* x, const void* target, double lr, double* loss);
+int fmoe_layer_sync_masters(fmoe_layer* layer);
+
 /* --------------------------------------------- expert parallelism (L2, EP) */
 /* A context's transport replaces the reference's Transport (transport.hpp:18-38).
  * Communicator over NCCL (NVLink/NVSwitch), one process per GPU: rank 0

@@ -467,6 +467,21 @@ class Ref(_Lib):
                   g("db2"), out["send_counts"], out["recv_counts"])
         return out
 
+    def train_steps(self, x, target, world, n, h, e_local, k, seed, steps, lr):
+        """ref_train_steps: the reference's train_step trajectory (x/target are
+        the rank-major [world*n, d] task)."""
+        x, target = _arr(x, np.float64), _arr(target, np.float64)
+        d = x.shape[1]
+        e = e_local * world
+        out = dict(losses=np.empty(steps), wg=np.empty((d, e)), w1=np.empty((e, d, h)), b1=np.empty((e, h)),
+                   w2=np.empty((e, h, d)), b2=np.empty((e, d)))
+        f = self.lib.ref_train_steps
+        f.restype = C.c_int
+        f.argtypes = [_i64] * 6 + [_u64, _i64, C.c_double] + [_vp] * 8
+        self.check(f(world, n, d, h, e_local, k, seed, steps, lr, _ptr(x), _ptr(target),
+                     *[_ptr(out[key]) for key in ("losses", "wg", "w1", "b1", "w2", "b2")]))
+        return out
+
     def exchange_counts(self, local_counts):
         lc = _arr(local_counts, np.int64)
         world, total = lc.shape

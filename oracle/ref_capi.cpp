@@ -336,6 +336,60 @@ int ref_moe_distributed(const double* x, const double* dy, int64_t world, int64_
   });
 }
 
+// train_step trajectories (moe_layer.cpp:144-205): `steps` SGD steps of the
+// reference's init_state(seed) layer on rank slices of x/target ([world*n, d]),
+// world ranks over its InProcWorld (world 1: no transport).  losses[steps] from
+// rank 0; final gate (rank 0) and every expert in global order.
+int ref_train_steps(int64_t world, int64_t n, int64_t d, int64_t h, int64_t e_local, int64_t k, uint64_t seed,
+                    int64_t steps, double lr, const double* x, const double* target, double* losses, double* wg,
+                    double* w1, double* b1, double* w2, double* b2) {
+  return guarded([&] {
+    MoEConfig cfg;
+    cfg.n_b = static_cast<std::size_t>(n);
+    cfg.d_m = static_cast<std::size_t>(d);
+    cfg.d_h = static_cast<std::size_t>(h);
+    cfg.k = static_cast<std::size_t>(k);
+    cfg.n_e_local = static_cast<std::size_t>(e_local);
+    cfg.world_size = static_cast<std::size_t>(world);
+    cfg.seed = seed;
+    auto run = [&](int r, Transport* t) {
+      MoELayerState st = init_state(cfg, r);
+      const Matrix xr = to_matrix(x + r * n * d, n, d), tr = to_matrix(target + r * n * d, n, d);
+      for (int64_t s = 0; s < steps; ++s) {
+        const double l = train_step(xr, tr, st, lr, t);
+        if (r == 0) losses[s] = l;
+      }
+      if (r == 0) out_matrix(st.gate.w_g, wg);
+      for (int64_t sl = 0; sl < e_local; ++sl) {
+        const int64_t g = r * e_local + sl;
+        out_matrix(st.experts[sl].w1, w1 + g * d * h);
+        out_matrix(st.experts[sl].b1, b1 + g * h);
+        out_matrix(st.experts[sl].w2, w2 + g * h * d);
+        out_matrix(st.experts[sl].b2, b2 + g * d);
+      }
+    };
+    if (world == 1) {
+      run(0, nullptr);
+      return;
+    }
+    InProcWorld w(static_cast<int>(world));
+    std::vector<std::exception_ptr> errs(static_cast<std::size_t>(world));
+    std::vector<std::thread> threads;
+    for (int64_t r = 0; r < world; ++r)
+      threads.emplace_back([&, r] {
+        try {
+          auto t = w.transport(static_cast<int>(r));
+          run(static_cast<int>(r), t.get());
+        } catch (...) {
+          errs[static_cast<std::size_t>(r)] = std::current_exception();
+        }
+      });
+    for (auto& th : threads) th.join();
+    for (auto& e : errs)
+      if (e) std::rethrow_exception(e);
+  });
+}
+
 // CPU-baseline handle: the reference's own init_state + forward/backward at a
 // given configuration, inputs from the bench generators (x stream 102, dy
 // stream 103; fmoe_bench.cpp:128-134,226-227).  Threads: FMOE_THREADS.

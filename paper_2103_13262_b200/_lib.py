@@ -78,7 +78,7 @@ EXPORTS = [
     "fmoe_comm_unique_id", "fmoe_comm_init", "fmoe_world_create", "fmoe_world_destroy",
     "fmoe_ctx_join_world", "fmoe_exchange_counts", "fmoe_ep_layout", "fmoe_a2a_rows",
     "fmoe_a2a_rows_reverse", "fmoe_allreduce_sum", "fmoe_matmul", "fmoe_softmax_rows", "fmoe_topk_rows",
-    "fmoe_experts_fwd_cached", "fmoe_experts_bwd_cached",
+    "fmoe_experts_fwd_cached", "fmoe_experts_bwd_cached", "fmoe_layer_train_step", "fmoe_layer_sync_masters",
 ]
 
 
@@ -134,6 +134,8 @@ def _load():
         "fmoe_comm_unique_id": [vp, i64],
         "fmoe_comm_init": [vp, vp, i64, C.c_int, C.c_int],
         "fmoe_allreduce_sum": [vp, C.c_int, vp, i64, vp, i64],
+        "fmoe_layer_train_step": [vp, vp, vp, C.c_double, C.POINTER(C.c_double)],
+        "fmoe_layer_sync_masters": [vp],
         "fmoe_matmul": [vp, C.c_int, vp, vp, i64, i64, i64, vp],
         "fmoe_softmax_rows": [vp, C.c_int, vp, i64, i64, vp],
         "fmoe_topk_rows": [vp, C.c_int, vp, i64, i64, i64, vp, vp],

@@ -574,6 +574,25 @@ class MoELayer:
         check(lib.fmoe_layer_bwd(self.h, _p(dy), _p(dx)))
         return dx
 
+    def train_step(self, x: torch.Tensor, target: torch.Tensor, lr: float) -> float:
+        """train_step (moe_layer.cpp:144-205) on device: forward, MSE against
+        target, backward, (EP) gradient sync, SGD.  Returns the world-average
+        loss (one host sync)."""
+        x, target = _dev(x), _dev(target)
+        shape = (self.config.n_b, self.config.d_m)
+        if x.shape != shape or target.shape != shape or x.dtype != self.dtype or target.dtype != self.dtype:
+            raise ShapeError(f"train_step: expected x and target [{shape[0]}, {shape[1]}] {self.dtype}")
+        self.ctx.use_current_stream()
+        loss = C.c_double()
+        check(lib.fmoe_layer_train_step(self.h, _p(x), _p(target), float(lr), C.byref(loss)))
+        self._x = x
+        return loss.value
+
+    def sync_masters(self):
+        """Re-widen the fp32 master weights of bf16 training from the bf16
+        parameters (after writing self.w_g / self.experts by hand)."""
+        check(lib.fmoe_layer_sync_masters(self.h))
+
     def step_host(self, x_host: torch.Tensor, dy_host: Optional[torch.Tensor], y_host: torch.Tensor,
                   dx_host: Optional[torch.Tensor] = None):
         """Host-buffer forward(+backward) through fmoe_layer_step_host."""

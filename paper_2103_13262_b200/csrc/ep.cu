@@ -300,6 +300,59 @@ __global__ void ordered_sum_kernel(const T* __restrict__ slabs, int64_t g, int64
   out[i] = acc;
 }
 
+void allreduce_sum(Ctx* c, fmoe_dtype dt, void* buf, int64_t n, const int* group, int64_t gs) {
+  if (dt != FMOE_F64 && dt != FMOE_F32) shape_error("allreduce_sum: dtype must be FMOE_F64 or FMOE_F32");
+  if (gs < 1 || !group) protocol_error("allreduce_sum: empty group");
+  for (int64_t i = 1; i < gs; ++i)
+    if (group[i] < group[i - 1]) protocol_error("allreduce_sum: group must be sorted ascending");
+  Transport* tr = c->transport;
+  const int W = tr ? tr->world : 1, r = tr ? tr->rank : 0;
+  int64_t me = -1;
+  for (int64_t i = 0; i < gs; ++i) {
+    if (group[i] < 0 || group[i] >= W) protocol_error("allreduce_sum: group rank outside the world");
+    if (group[i] == r) me = i;
+  }
+  if (me < 0) protocol_error("allreduce_sum: calling rank not in group");
+  if (gs == 1) return;
+  const size_t es = dtype_size(dt);
+  // phase 1: element counts, so a shape mismatch is a ProtocolError on every
+  // member instead of a mismatched transfer
+  int64_t* cnt = (int64_t*)ctx_workspace(c, (size_t)(gs + 1) * 8 + (size_t)gs * n * es + 512);
+  uint8_t* slabs = (uint8_t*)cnt + ((size_t)(gs + 1) * 8 + 255) / 256 * 256;
+  std::vector<int64_t> h(gs, n);
+  CK(cudaMemcpyAsync(cnt + gs, &n, 8, cudaMemcpyHostToDevice, c->stream));
+  std::vector<Xfer> sends, recvs;
+  for (int64_t i = 0; i < gs; ++i) {
+    if (i == me) continue;
+    sends.push_back({group[i], cnt + gs, 8});
+    recvs.push_back({group[i], cnt + i, 8});
+  }
+  tr->group(c, sends, recvs);
+  CK(cudaMemcpyAsync(h.data(), cnt, gs * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  h[me] = n;
+  for (int64_t i = 0; i < gs; ++i)
+    if (h[i] != n)
+      protocol_error("allreduce_sum: rank " + std::to_string(group[i]) + " contributes " + std::to_string(h[i]) +
+                     " elements, this rank " + std::to_string(n));
+  if (n == 0) return;
+  // phase 2: all-gather into [gs][n] slabs in group order, then the ordered sum
+  sends.clear();
+  recvs.clear();
+  for (int64_t i = 0; i < gs; ++i) {
+    if (i == me) continue;
+    sends.push_back({group[i], buf, (size_t)n * es});
+    recvs.push_back({group[i], slabs + (size_t)i * n * es, (size_t)n * es});
+  }
+  CK(cudaMemcpyAsync(slabs + (size_t)me * n * es, buf, (size_t)n * es, cudaMemcpyDeviceToDevice, c->stream));
+  tr->group(c, sends, recvs);
+  const unsigned grid = (unsigned)ceil_div(n, 256);
+  if (dt == FMOE_F64)
+    fmoe_b200::ordered_sum_kernel<double><<<grid, 256, 0, c->stream>>>((const double*)slabs, gs, n, (double*)buf);
+  else
+    fmoe_b200::ordered_sum_kernel<float><<<grid, 256, 0, c->stream>>>((const float*)slabs, gs, n, (float*)buf);
+  CK_LAUNCH(c);
+}
 }  // namespace fmoe_b200
 
 namespace {
@@ -358,59 +411,6 @@ void a2a(Ctx* c, fmoe_dtype dt, const void* src, int64_t d, const fmoe_exchange_
   exchange_rows(c, tr, P, (size_t)d * dtype_size(dt), src, dst, fwd);
 }
 
-void allreduce(Ctx* c, fmoe_dtype dt, void* buf, int64_t n, const int* group, int64_t gs) {
-  if (dt != FMOE_F64 && dt != FMOE_F32) shape_error("allreduce_sum: dtype must be FMOE_F64 or FMOE_F32");
-  if (gs < 1 || !group) protocol_error("allreduce_sum: empty group");
-  for (int64_t i = 1; i < gs; ++i)
-    if (group[i] < group[i - 1]) protocol_error("allreduce_sum: group must be sorted ascending");
-  Transport* tr = c->transport;
-  const int W = tr ? tr->world : 1, r = tr ? tr->rank : 0;
-  int64_t me = -1;
-  for (int64_t i = 0; i < gs; ++i) {
-    if (group[i] < 0 || group[i] >= W) protocol_error("allreduce_sum: group rank outside the world");
-    if (group[i] == r) me = i;
-  }
-  if (me < 0) protocol_error("allreduce_sum: calling rank not in group");
-  if (gs == 1) return;
-  const size_t es = dtype_size(dt);
-  // phase 1: element counts, so a shape mismatch is a ProtocolError on every
-  // member instead of a mismatched transfer
-  int64_t* cnt = (int64_t*)ctx_workspace(c, (size_t)(gs + 1) * 8 + (size_t)gs * n * es + 512);
-  uint8_t* slabs = (uint8_t*)cnt + ((size_t)(gs + 1) * 8 + 255) / 256 * 256;
-  std::vector<int64_t> h(gs, n);
-  CK(cudaMemcpyAsync(cnt + gs, &n, 8, cudaMemcpyHostToDevice, c->stream));
-  std::vector<Xfer> sends, recvs;
-  for (int64_t i = 0; i < gs; ++i) {
-    if (i == me) continue;
-    sends.push_back({group[i], cnt + gs, 8});
-    recvs.push_back({group[i], cnt + i, 8});
-  }
-  tr->group(c, sends, recvs);
-  CK(cudaMemcpyAsync(h.data(), cnt, gs * 8, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  h[me] = n;
-  for (int64_t i = 0; i < gs; ++i)
-    if (h[i] != n)
-      protocol_error("allreduce_sum: rank " + std::to_string(group[i]) + " contributes " + std::to_string(h[i]) +
-                     " elements, this rank " + std::to_string(n));
-  if (n == 0) return;
-  // phase 2: all-gather into [gs][n] slabs in group order, then the ordered sum
-  sends.clear();
-  recvs.clear();
-  for (int64_t i = 0; i < gs; ++i) {
-    if (i == me) continue;
-    sends.push_back({group[i], buf, (size_t)n * es});
-    recvs.push_back({group[i], slabs + (size_t)i * n * es, (size_t)n * es});
-  }
-  CK(cudaMemcpyAsync(slabs + (size_t)me * n * es, buf, (size_t)n * es, cudaMemcpyDeviceToDevice, c->stream));
-  tr->group(c, sends, recvs);
-  const unsigned grid = (unsigned)ceil_div(n, 256);
-  if (dt == FMOE_F64)
-    fmoe_b200::ordered_sum_kernel<double><<<grid, 256, 0, c->stream>>>((const double*)slabs, gs, n, (double*)buf);
-  else
-    fmoe_b200::ordered_sum_kernel<float><<<grid, 256, 0, c->stream>>>((const float*)slabs, gs, n, (float*)buf);
-  CK_LAUNCH(c);
-}
 }  // namespace
 
 extern "C" {
@@ -514,7 +514,7 @@ int fmoe_a2a_rows(fmoe_ctx* ctx, fmoe_dtype dtype, const void* xs, int64_t d, co
 
 int fmoe_allreduce_sum(fmoe_ctx* ctx, fmoe_dtype dtype, void* buf, int64_t n, const int* group,
                        int64_t group_size) {
-  FMOE_GUARD(allreduce(CX(ctx), dtype, buf, n, group, group_size))
+  FMOE_GUARD(allreduce_sum(CX(ctx), dtype, buf, n, group, group_size))
 }
 
 int fmoe_a2a_rows_reverse(fmoe_ctx* ctx, fmoe_dtype dtype, const void* ys, int64_t d,

@@ -139,6 +139,7 @@ void Layer::init_weights() {
   upload(c1, b1, bias_t);
   upload(a2, w2, t);
   upload(c2, b2, bias_t);
+  masters_fresh = false;  // bf16 training re-widens its fp32 masters
 }
 
 void Layer::forward(const void* x, void* y) {

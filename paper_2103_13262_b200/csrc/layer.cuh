@@ -34,6 +34,12 @@ struct Layer {
   // host-buffer step
   void* io = nullptr;
   void* h_stage = nullptr;
+  // training step (train.cu): output, d_y, d_x, loss scratch; fp32 masters of
+  // the bf16 weights (widened on the first step after init / an explicit resync)
+  void *t_y = nullptr, *t_dy = nullptr, *t_dx = nullptr;
+  double* t_loss = nullptr;
+  float *m_wg = nullptr, *m_w1 = nullptr, *m_w2 = nullptr;
+  bool masters_fresh = false;
   // expert parallelism (ep.cu)
   struct Ep;
   Ep* ep = nullptr;
@@ -45,6 +51,8 @@ struct Layer {
   void init_weights();
   void forward(const void* x, void* y);
   void backward(const void* dy, void* dx);
+  double train_step(const void* x, const void* target, double lr);
+  void sgd(void* param, float* master, const void* grad, int64_t n, double lr, bool weight);
   void step_host(const void* x_host, const void* dy_host, void* y_host, void* dx_host);
   void ep_alloc();
   void ep_check() const;  // ProtocolError unless a matching transport is attached

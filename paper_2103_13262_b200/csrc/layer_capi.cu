@@ -75,6 +75,16 @@ int fmoe_layer_bwd(fmoe_layer* layer, const void* dy, void* dx) {
   })
 }
 
+int fmoe_layer_train_step(fmoe_layer* layer, const void* x, const void* target, double lr, double* loss) {
+  FMOE_GUARD({
+    if (!x || !target) shape_error("train_step: null x or target");
+    const double v = L(layer)->train_step(x, target, lr);
+    if (loss) *loss = v;
+  })
+}
+
+int fmoe_layer_sync_masters(fmoe_layer* layer) { FMOE_GUARD(L(layer)->masters_fresh = false) }
+
 int fmoe_layer_step_host(fmoe_layer* layer, const void* x_host, const void* dy_host, void* y_host,
                          void* dx_host) {
   FMOE_GUARD({

@@ -38,6 +38,9 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
                  const fmoe_expert_params& w, const void* xs, const void* hidden, const void* d_ys,
                  void* d_xs, const fmoe_expert_grads& g, void* d_pre_ws, float* part_ws,
                  const uint32_t* relu_bits = nullptr, const void* mask = nullptr);
+// allreduce_sum over ctx's transport (ep.cu): in place, ascending-rank order.
+void allreduce_sum(Ctx* c, fmoe_dtype dt, void* buf, int64_t n, const int* group, int64_t gs);
+
 // fp32 scratch floats experts_bwd needs for the bf16 bias-gradient partials
 int64_t experts_bwd_part_floats(const fmoe_plan& b, int64_t d, int64_t h);
 

@@ -1,0 +1,135 @@
+"""Device training step (fmoe_layer_train_step; train_step, moe_layer.cpp:144-205).
+
+* fp64: 10-step SGD trajectories (losses and every parameter) match the
+  reference's own train_step (oracle/_ref, ref_train_steps) on one rank and on
+  an expert-parallel world of 2 ranks (in-process world, one thread per rank),
+  and the world-2 run matches the world-1 run (test_moe_layer.cpp:364-411).
+* bf16: lr = 0 reports the MSE and leaves the parameters bit-identical; the
+  toy regression's loss falls; the fp32 masters keep updates that bf16 alone
+  would round away.
+"""
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fm():
+    import paper_2103_13262_b200 as m
+
+    return m
+
+
+def _task(world, n, d, seed=9):
+    g = np.random.default_rng(seed)
+    x = g.uniform(-1, 1, (world * n, d))
+    t = x @ g.uniform(-0.5, 0.5, (d, d)) + 0.1 * x * x
+    return x, t
+
+
+def _params(layer):
+    f = lambda v: v.detach().cpu().double().numpy()  # noqa: E731
+    e = layer.experts
+    return dict(wg=f(layer.w_g), w1=f(e.w1), b1=f(e.b1), w2=f(e.w2), b2=f(e.b2))
+
+
+def _train(fm, cfg, rank, dtype, x, t, steps, lr, world_obj=None):
+    layer = fm.MoELayer(cfg, rank=rank, dtype=dtype)
+    if world_obj is not None:
+        layer.join(world_obj)
+    xd = torch.as_tensor(x).to(device="cuda", dtype=dtype)
+    td = torch.as_tensor(t).to(device="cuda", dtype=dtype)
+    losses = [layer.train_step(xd, td, lr) for _ in range(steps)]
+    torch.cuda.synchronize()
+    return losses, _params(layer)
+
+
+def _train_world(fm, world, n, d, h, el, k, seed, x, t, steps, lr):
+    w = fm.World(world)
+    res, errs = [None] * world, [None] * world
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                res[r] = _train(fm, fm.MoEConfig(n, d, h, k, el, world, seed), r, torch.float64,
+                                x[r * n:(r + 1) * n], t[r * n:(r + 1) * n], steps, lr, w)
+                s.synchronize()
+        except Exception as e:  # noqa: BLE001
+            errs[r] = e
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    [a.start() for a in th]
+    [a.join(timeout=300) for a in th]
+    for e in errs:
+        if e is not None:
+            raise e
+    return res
+
+
+def _close(a, b, tol):
+    return float(np.max(np.abs(np.asarray(a) - np.asarray(b)))) <= tol
+
+
+def test_f64_trajectory_matches_reference(fm, ref):
+    n, d, h, el, k, seed, steps, lr = 64, 24, 40, 8, 2, 11, 10, 0.05
+    x, t = _task(1, n, d)
+    losses, p = _train(fm, fm.MoEConfig(n, d, h, k, el, 1, seed), 0, torch.float64, x, t, steps, lr)
+    r = ref.train_steps(x, t, 1, n, h, el, k, seed, steps, lr)
+    # bit-identical arithmetic except the softmax exp (a few ulp)
+    assert _close(losses, r["losses"], 1e-13 * max(1.0, abs(r["losses"][0]))), (losses, r["losses"])
+    for key in ("wg", "w1", "b1", "w2", "b2"):
+        assert _close(p[key].reshape(r[key].shape), r[key], 1e-13), key
+    assert losses[-1] < losses[0]
+
+
+def test_f64_ep_trajectory_matches_reference_and_world1(fm, ref):
+    world, n, d, h, el, k, seed, steps, lr = 2, 16, 12, 20, 4, 2, 20, 10, 0.01
+    x, t = _task(world, n, d, seed=4)
+    res = _train_world(fm, world, n, d, h, el, k, seed, x, t, steps, lr)
+    r = ref.train_steps(x, t, world, n, h, el, k, seed, steps, lr)
+    for rank in range(world):
+        losses, p = res[rank]
+        assert losses == res[0][0]  # every rank reports the same world loss
+        assert _close(losses, r["losses"], 1e-13), (losses, r["losses"])
+        assert _close(p["wg"], r["wg"], 1e-13)
+        sl = slice(rank * el, (rank + 1) * el)
+        for key in ("w1", "b1", "w2", "b2"):
+            assert _close(p[key], r[key][sl], 1e-13), key
+    # the reference's own criterion: world 2 follows the world-1 trajectory
+    one, p1 = _train(fm, fm.MoEConfig(world * n, d, h, k, world * el, 1, seed), 0, torch.float64, x, t, steps, lr)
+    assert _close(res[0][0], one, 1e-8)
+    assert _close(res[0][1]["wg"], p1["wg"], 1e-8)
+    assert _close(np.concatenate([res[rk][1]["w1"] for rk in range(world)]), p1["w1"], 1e-8)
+
+
+def test_bf16_zero_lr_reports_mse_and_keeps_parameters(fm):
+    n, d, h, e, k = 512, 128, 256, 16, 2
+    x, t = _task(1, n, d, seed=2)
+    layer = fm.MoELayer(fm.MoEConfig(n, d, h, k, e, 1, 3), dtype=torch.bfloat16)
+    before = {key: v.copy() for key, v in _params(layer).items()}
+    xd = torch.as_tensor(x).to(device="cuda", dtype=torch.bfloat16)
+    td = torch.as_tensor(t).to(device="cuda", dtype=torch.bfloat16)
+    y = layer.forward(xd).double()
+    want = float(((y - td.double()) ** 2).mean())
+    loss = layer.train_step(xd, td, 0.0)
+    assert abs(loss - want) <= 1e-9 * want
+    after = _params(layer)
+    for key in before:
+        assert np.array_equal(before[key], after[key]), key
+
+
+def test_bf16_training_reduces_loss(fm):
+    n, d, h, e, k = 1024, 128, 256, 16, 2
+    x, t = _task(1, n, d, seed=6)
+    losses, _ = _train(fm, fm.MoEConfig(n, d, h, k, e, 1, 7), 0, torch.bfloat16, x, t, 30, 0.5)
+    assert all(np.isfinite(losses))
+    # the loss is a mean over n*d elements, so per-step changes are small but
+    # steady; bf16 weights without fp32 masters would stall on rounding
+    assert all(b < a for a, b in zip(losses, losses[1:])), losses
+    assert losses[-1] < losses[0] * (1 - 5e-4), losses
