@@ -34,6 +34,29 @@ METRIC = "MoE-layer fwd+bwd tokens/s at 1/2/4/8 B200; expert-GEMM % of tensor pe
 UNIT = "tokens/s"
 CFG2 = dict(n_b=65536, d_m=1024, d_h=4096, n_e_local=64, k=2)          # 1 GPU
 CFG3 = dict(n_b=16384, d_m=2048, d_h=8192, n_e_local=8, k=2)           # EP, per GPU
+CFG4_LAYERS = 12
+ZIPF_S = 1.0
+
+
+def workload_cfg(name: str, world: int) -> dict:
+    """Per-GPU shape of a BASELINE workload at `world` GPUs."""
+    if name == "cfg2":
+        if world != 1:
+            raise SystemExit("cfg2 is the single-GPU workload (use cfg3/cfg4/cfg5 at N>1)")
+        return dict(CFG2)
+    if name == "cfg3":
+        return dict(CFG3)
+    if name == "cfg4":  # 12-layer stack, 128 experts over the world, 16384 tokens/GPU
+        if 128 % world:
+            raise SystemExit("cfg4 needs the world size to divide 128 experts")
+        return dict(n_b=16384, d_m=1024, d_h=4096, n_e_local=128 // world, k=2)
+    if name == "cfg5":  # Zipf routing, 256 experts top-1, 262144 tokens in total
+        if 256 % world:
+            raise SystemExit("cfg5 needs the world size to divide 256 experts")
+        return dict(n_b=262144 // world, d_m=1024, d_h=4096, n_e_local=256 // world, k=1)
+    raise SystemExit(f"unknown workload {name}")
+
+
 SEED = 42
 STAGES = ["-", "gate", "plan", "scatter", "fc1", "fc2", "gather_combine", "fwd_bwd_gap",
           "gather_combine_bwd", "dgrad_fc2", "wgrad_fc2", "db2", "dgrad_fc1", "wgrad_fc1", "db1",
@@ -91,38 +114,61 @@ class Clocks:
 
 
 # ------------------------------------------------------------- CPU reference
-def cpu_reference(n_tokens: int, cfg: dict, min_seconds: float = 10.0, max_reps: int = 5):
+def cpu_reference(n_tokens: int, cfg: dict, min_seconds: float = 10.0, max_reps: int = 5,
+                  workload: str = "cfg2", n_layers: int = 1, e_total: int = 0):
     """The reference's own forward+backward (oracle/_ref, compiled from its
-    sources) on the host cores: tokens/s on a bounded token sample of cfg."""
+    sources) on the host cores: tokens/s on a bounded token sample of the
+    workload's layer (all e_total experts on one worker).  cfg5 feeds the same
+    Zipf IndexMatrix to the reference's dispatch + expert pool; cfg4 divides
+    the one-layer rate by the stack depth."""
     cores = os.cpu_count() or 1
     os.environ["FMOE_THREADS"] = str(cores)
     from oracle import bindings
 
     if not bindings.ref_available():
         return None
+    e_total = e_total or cfg["n_e_local"]
     lib = C.CDLL(bindings.REF_SO)
-    lib.ref_bench_create.restype = C.c_void_p
-    lib.ref_bench_create.argtypes = [C.c_uint64] + [C.c_int64] * 5
-    lib.ref_bench_step.argtypes = [C.c_void_p]
-    lib.ref_bench_destroy.argtypes = [C.c_void_p]
-    h = lib.ref_bench_create(SEED, n_tokens, cfg["d_m"], cfg["d_h"], cfg["n_e_local"], cfg["k"])
+    routed = workload == "cfg5"
+    if routed:
+        import numpy as np
+
+        from paper_2103_13262_b200.workloads import zipf_routing
+
+        idx, sc = zipf_routing(n_tokens, e_total, cfg["k"], ZIPF_S, seed=7)
+        idx64 = np.ascontiguousarray(idx, dtype=np.int64)
+        sc64 = np.ascontiguousarray(sc, dtype=np.float64)
+        create, step, destroy = lib.ref_bench_routed_create, lib.ref_bench_routed_step, lib.ref_bench_routed_destroy
+        create.argtypes = [C.c_uint64] + [C.c_int64] * 5 + [C.c_void_p, C.c_void_p]
+        extra = (idx64.ctypes.data, sc64.ctypes.data)
+    else:
+        create, step, destroy = lib.ref_bench_create, lib.ref_bench_step, lib.ref_bench_destroy
+        create.argtypes = [C.c_uint64] + [C.c_int64] * 5
+        extra = ()
+    create.restype = C.c_void_p
+    step.argtypes = [C.c_void_p]
+    destroy.argtypes = [C.c_void_p]
+    h = create(SEED, n_tokens, cfg["d_m"], cfg["d_h"], e_total, cfg["k"], *extra)
     if not h:
         return None
     try:
-        lib.ref_bench_step(h)  # warm-up
+        step(h)  # warm-up
         times = []
         t_all = time.perf_counter()
         while len(times) < max_reps and (len(times) < 2 or time.perf_counter() - t_all < min_seconds):
             t0 = time.perf_counter()
-            lib.ref_bench_step(h)
+            step(h)
             times.append(time.perf_counter() - t0)
     finally:
-        lib.ref_bench_destroy(h)
+        destroy(h)
     mean = statistics.mean(times)
-    return {"value": n_tokens / mean, "unit": UNIT, "cores": cores, "kind": "reference",
-            "sample": (f"{n_tokens} tokens of d_m={cfg['d_m']} d_h={cfg['d_h']} E={cfg['n_e_local']} "
+    what = ("Zipf-routed dispatch + expert pool (build_plan .. scatter_backward)" if routed
+            else "forward+backward")
+    stack = f", rate / {n_layers} layers" if n_layers > 1 else ""
+    return {"value": n_tokens / mean / n_layers, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": (f"{n_tokens} tokens of d_m={cfg['d_m']} d_h={cfg['d_h']} E={e_total} "
                        f"k={cfg['k']} (the GPU workload's layer, token-subsampled), fp64, reference "
-                       f"forward+backward, warm-up 1 + {len(times)} reps, mean {mean:.2f} s/step, "
+                       f"{what}{stack}, warm-up 1 + {len(times)} reps, mean {mean:.2f} s/step, "
                        f"FMOE_THREADS={cores}")}
 
 
@@ -134,46 +180,68 @@ def cpu_tokens_for(cores: int) -> int:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="default", choices=["default", "cfg2", "cfg3", "cfg4", "cfg5"],
+                    help="BASELINE config (SURVEY §8d); default: cfg2 at N=1, cfg3 at N>1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0)
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    cfg = CFG2 if world == 1 else CFG3
+    if args.workload == "default":
+        args.workload = "cfg2" if world == 1 else "cfg3"
+    cfg = workload_cfg(args.workload, world)
     if args.impl == "reference":
         return run_reference(args, world, rank, cfg)
     return run_ours(args, world, rank, cfg)
+
+
+def n_layers_of(workload: str) -> int:
+    return CFG4_LAYERS if workload == "cfg4" else 1
+
+
+def cpu_sample_tokens(workload: str, cores: int) -> int:
+    n = cpu_tokens_for(cores)
+    return max(256, n // 4) if workload == "cfg4" else n
 
 
 def run_reference(args, world, rank, cfg):
     if rank != 0:
         return 0
     cores = os.cpu_count() or 1
-    res = cpu_reference(cpu_tokens_for(cores), cfg, min_seconds=max(10.0, 2.0 * args.steps),
-                        max_reps=max(2, min(args.steps, 10)))
+    n_tok = cpu_sample_tokens(args.workload, cores)
+    res = cpu_reference(n_tok, cfg, min_seconds=max(10.0, 2.0 * args.steps),
+                        max_reps=max(2, min(args.steps, 10)), workload=args.workload,
+                        n_layers=n_layers_of(args.workload), e_total=cfg["n_e_local"] * world)
     if res is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libfmoe_ref.so not built"}))
         return 0
     line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "ms_per_step": 1e3 * cpu_tokens_for(cores) / res["value"], "dtype": "f64", "data": "synthetic",
+            "ms_per_step": 1e3 * cfg["n_b"] * world / res["value"], "dtype": "f64", "data": "synthetic",
             "scaling": "weak", "vs_baseline": None,
-            "config": {"workload": workload_name(cfg, world), **cfg, "world": world},
+            "config": {"workload": workload_name(args.workload, cfg, world), **cfg, "world": world},
             "cpu_baseline": res,
             "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
 
 
-def workload_name(cfg, world):
-    if world == 1:
+def workload_name(workload, cfg, world):
+    if workload == "cfg2":
         return ("cfg2: single MoE layer d_model=1024 d_hidden=4096, 64 experts top-2, 65536 tokens, "
                 "bf16 storage / fp32 accumulate, fwd+bwd")
-    return (f"cfg3: expert-parallel MoE layer d_model=2048 d_hidden=8192, 8 experts/GPU x {world} GPUs, "
-            "top-2, 16384 tokens/GPU, fwd+bwd")
+    if workload == "cfg3":
+        return (f"cfg3: expert-parallel MoE layer d_model=2048 d_hidden=8192, 8 experts/GPU x {world} GPUs, "
+                "top-2, 16384 tokens/GPU, fwd+bwd")
+    if workload == "cfg4":
+        return (f"cfg4: GPT-style MoE FFN stack, {CFG4_LAYERS} chained layers (no residual/norm, as the "
+                f"reference), d_model=1024 d_hidden=4096, 128 experts top-2 over {world} GPU(s), "
+                "16384 tokens/GPU, fwd through all layers then bwd")
+    return (f"cfg5: skewed-gate stress, injected Zipf(s={ZIPF_S}) routing over 256 experts top-1, "
+            f"262144 tokens in total ({cfg['n_b']}/GPU), d_model=1024 d_hidden=4096, fwd+bwd")
 
 
 def run_ours(args, world, rank, cfg):
@@ -188,29 +256,45 @@ def run_ours(args, world, rank, cfg):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2103_13262_b200 as fm
     from paper_2103_13262_b200 import _lib
+    from paper_2103_13262_b200.workloads import MoEStack, zipf_routing
 
+    wl = args.workload
+    n_layers = n_layers_of(wl)
     n, d, h, el, k = cfg["n_b"], cfg["d_m"], cfg["d_h"], cfg["n_e_local"], cfg["k"]
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
-        layer = fm.MoELayer(fm.MoEConfig(n, d, h, k, el, world, SEED), rank=rank, dtype=torch.bfloat16)
+        mcfg = fm.MoEConfig(n, d, h, k, el, world, SEED)
+        if wl == "cfg4":
+            model = MoEStack(mcfg, n_layers, rank=rank, dtype=torch.bfloat16)
+            layer0 = model.layers[0]
+        else:
+            model = layer0 = fm.MoELayer(mcfg, rank=rank, dtype=torch.bfloat16)
         if world > 1:
-            layer.connect(dist)
+            model.connect(dist)
         g = torch.Generator(device="cuda")
         g.manual_seed(1000 + rank)
         x = (torch.rand(n, d, device="cuda", generator=g) * 2 - 1).bfloat16()
         dy = (torch.rand(n, d, device="cuda", generator=g) * 2 - 1).bfloat16()
         y = torch.empty_like(x)
         dx = torch.empty_like(x)
+        if wl == "cfg5":
+            ridx, rsc = zipf_routing(n, el * world, k, ZIPF_S, seed=7 + rank)
+            ridx = torch.as_tensor(ridx, device="cuda")
+            rsc = torch.as_tensor(rsc, device="cuda")
 
-        def step():
-            layer.forward(x, y)
-            layer.backward(dy, dx)
+            def step():
+                model.forward_routed(x, ridx, rsc, y)
+                model.backward(dy, dx)
+        else:
+            def step():
+                model.forward(x, y)
+                model.backward(dy, dx)
 
         clocks = Clocks(local)  # sampled from the warm-up (under load) through the timed region
-        for _ in range(max(args.warmup, 3) if args.warmup >= 0 else 3):
+        for _ in range(max(args.warmup, 3)):
             step()
-        ctx = layer.ctx
-        _lib.check(_lib.lib.fmoe_ctx_profile(ctx.h, args.steps))
+        ctx = layer0.ctx
+        _lib.check(_lib.lib.fmoe_ctx_profile(ctx.h, args.steps * n_layers))
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
@@ -232,6 +316,7 @@ def run_ours(args, world, rank, cfg):
         done = C.c_int()
         _lib.check(_lib.lib.fmoe_ctx_profile_read(ctx.h, stage, len(STAGES), C.byref(done)))
         _lib.check(_lib.lib.fmoe_ctx_profile(ctx.h, 0))
+        # per layer-step averages
         stage_ms = {STAGES[i]: stage[i] / max(done.value, 1) for i in range(1, len(STAGES))}
         if dist:
             t = torch.tensor([ms], device="cuda", dtype=torch.float64)
@@ -240,37 +325,45 @@ def run_ours(args, world, rank, cfg):
         tokens = n * world
         value = tokens / (ms / 1e3)
 
-        # ---- end to end through the public host-buffer entry point
-        e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
-        hx = x.cpu().pin_memory()
-        hdy = dy.cpu().pin_memory()
-        hy = torch.empty_like(hx).pin_memory()
-        hdx = torch.empty_like(hx).pin_memory()
-        layer.step_host(hx, hdy, hy, hdx)
-        if dist:
-            dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for _ in range(e2e_steps):
-            layer.step_host(hx, hdy, hy, hdx)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = e0.elapsed_time(e1) / e2e_steps
-        if dist:
-            t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+        # ---- end to end through the public host-buffer entry point (single layers)
+        e2e = None
+        if wl in ("cfg2", "cfg3"):
+            e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
+            hx = x.cpu().pin_memory()
+            hdy = dy.cpu().pin_memory()
+            hy = torch.empty_like(hx).pin_memory()
+            hdx = torch.empty_like(hx).pin_memory()
+            layer0.step_host(hx, hdy, hy, hdx)
+            if dist:
+                dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(e2e_steps):
+                layer0.step_host(hx, hdy, hy, hdx)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            e2e_ms = e0.elapsed_time(e1) / e2e_steps
+            if dist:
+                t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                e2e_ms = float(t.item())
+            e2e = {"value": tokens / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 2 * n * d * 2,
+                   "d2h_bytes_per_step": 2 * n * d * 2,
+                   "path": ("fmoe_layer_step_host (pinned host x,dy -> H2D -> fwd+bwd -> D2H y,dx; "
+                            "dy upload / y, dx download overlapped with the kernels on copy streams)")}
 
     pk = peaks()
-    flop_gemm = 2.0 * n * k * d * h  # one expert GEMM launch (fmoe_bench.cpp:110-126)
+    # expert GEMM FLOPs of one launch (fmoe_bench.cpp:110-126): 2 * rows * d * h,
+    # rows = tokens routed to this rank's experts (N*k per rank on average)
+    flop_gemm = 2.0 * n * k * d * h
     gemm_ms = [stage_ms[s] for s in GEMM_STAGES]
     avg_launch_ms = sum(gemm_ms) / len(gemm_ms)
     achieved = flop_gemm / (avg_launch_ms / 1e3) / 1e12
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and wl == "cfg2":
         try:
             traffic = json.load(open(tp)).get("tc_gemm_dram_bytes_per_launch")
         except Exception:
@@ -281,16 +374,15 @@ def run_ours(args, world, rank, cfg):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform[-1,1) inputs; reference init_state weights)",
-        "config": {"workload": workload_name(cfg, world), "n_b_per_gpu": n, "d_m": d, "d_h": h,
-                   "experts_per_gpu": el, "experts_total": el * world, "k": k,
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (uniform[-1,1) inputs; reference init_state weights"
+                + ("; injected Zipf routing" if wl == "cfg5" else "") + ")",
+        "config": {"workload": workload_name(wl, cfg, world), "n_b_per_gpu": n, "d_m": d, "d_h": h,
+                   "experts_per_gpu": el, "experts_total": el * world, "k": k, "layers": n_layers,
                    "parallelism": f"ep{world}" if world > 1 else "single",
-                   "l2": "working set ~7 GB >> 126 MB L2; no flush needed"},
+                   "l2": "working set several GB >> 126 MB L2; no flush needed"},
         "gpu_launches": launches,
         "clocks": clk,
-        "e2e": {"value": tokens / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 2 * n * d * 2,
-                "d2h_bytes_per_step": 2 * n * d * 2,
-                "path": "fmoe_layer_step_host (pinned host x,dy -> H2D -> fwd+bwd -> D2H y,dx)"},
         "roofline": {"kernel": "tc_gemm_kernel (grouped tcgen05 expert GEMM; fc1, fc2, 2x dgrad, 2x wgrad)",
                      "bound": "tensor", "achieved": achieved, "peak": pk["tc_sus"], "unit": "TFLOP/s",
                      "frac": achieved / pk["tc_sus"], "frac_of_burst_peak": achieved / pk["tc"],
@@ -299,16 +391,24 @@ def run_ours(args, world, rank, cfg):
                      "peak_source": pk["src"] + " bf16 sustained (kernel timed inside a long step)"},
         "stages_ms": {k_: round(v, 4) for k_, v in stage_ms.items()},
         "permute_roofline": {
-            "scatter_GBps": scatter_bytes / (stage_ms["scatter"] / 1e3) / 1e9,
-            "gather_combine_GBps": gather_bytes / (stage_ms["gather_combine"] / 1e3) / 1e9,
+            "scatter_GBps": scatter_bytes / (stage_ms["scatter"] / 1e3) / 1e9 if stage_ms["scatter"] > 0 else None,
+            "gather_combine_GBps": (gather_bytes / (stage_ms["gather_combine"] / 1e3) / 1e9
+                                    if stage_ms["gather_combine"] > 0 else None),
             "peak_GBps": pk["hbm"],
         },
     }
-    line["permute_roofline"]["scatter_frac"] = line["permute_roofline"]["scatter_GBps"] / pk["hbm"]
-    line["permute_roofline"]["gather_frac"] = line["permute_roofline"]["gather_combine_GBps"] / pk["hbm"]
+    if e2e is not None:
+        line["e2e"] = e2e
+    pr = line["permute_roofline"]
+    if world == 1 and pr["scatter_GBps"]:
+        pr["scatter_frac"] = pr["scatter_GBps"] / pk["hbm"]
+        pr["gather_frac"] = pr["gather_combine_GBps"] / pk["hbm"]
+    else:
+        pr["note"] = "under EP the scatter / gather stages include the NCCL exchanges"
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
-        line["cpu_baseline"] = cpu_reference(cpu_tokens_for(cores), cfg)
+        line["cpu_baseline"] = cpu_reference(cpu_sample_tokens(wl, cores), cfg, workload=wl, n_layers=n_layers,
+                                             e_total=el * world)
     if rank == 0:
         print(json.dumps(line))
     if dist:

@@ -221,6 +221,18 @@ int fmoe_layer_routing(fmoe_layer* layer, const int32_t** topk_idx, const void**
 int fmoe_layer_fwd(fmoe_layer* layer, const void* x, void* y);
 /* backward (moe_layer.cpp:112-142): dy -> dx and parameter gradients. */
 int fmoe_layer_bwd(fmoe_layer* layer, const void* dy, void* dx);
+/* forward with injected routing (the skewed-gate stress of SURVEY §8d cfg5:
+ * a sampled IndexMatrix fed straight into build_plan, dispatch.hpp:28):
+ * topk_idx [n_b, k] int32 in [0, E) (out of range -> ShapeError at
+ * fmoe_ctx_check, as build_plan, dispatch.cpp:21-23), topk_scores [n_b, k]
+ * in the score dtype.  The gate is skipped; the following fmoe_layer_bwd
+ * yields d_x = scatter_backward(d_xs) (dispatch.cpp:80-95) with no gate term,
+ * a zero gate gradient, and d(topk_scores) (gather_combine_backward's d_w,
+ * dispatch.cpp:97-126) through fmoe_layer_routing_grad. */
+int fmoe_layer_fwd_routed(fmoe_layer* layer, const void* x, const int32_t* topk_idx, const void* topk_scores,
+                          void* y);
+/* d(topk_scores) [n_b, k] of the last backward (score dtype, device). */
+int fmoe_layer_routing_grad(fmoe_layer* layer, const void** d_topk_scores);
 /* Host-buffer step for end-to-end use: H2D x (and dy), forward, backward,
  * D2H y (and dx).  Buffers are host memory (pinned for full speed); dy/dx may
  * be NULL for forward only.  Synchronises before returning. */
@@ -255,6 +267,36 @@ typedef struct fmoe_world fmoe_world;
 int fmoe_world_create(int world, fmoe_world** out);
 int fmoe_world_destroy(fmoe_world* world);
 int fmoe_ctx_join_world(fmoe_ctx* ctx, fmoe_world* world, int rank);
+
+/* How an expert-parallel bf16 layer moves its rows (the reference's
+ * all_to_all_rows / _reverse, collectives.cpp:146-265):
+ *   FMOE_EP_EXCHANGE_PEER (default): fused into the kernels over NVLink peer
+ *     memory -- the scatter writes token rows into the expert ranks, the fc2 /
+ *     dgrad-fc1 epilogues store rows back into the source ranks, epoch flags
+ *     in peer memory order the phases.  Connected on the first step through
+ *     the context's transport (raw pointers inside one process, CUDA IPC
+ *     across processes); if any rank cannot map its peers, every rank keeps
+ *     the transport exchange.
+ *   FMOE_EP_EXCHANGE_TRANSPORT: grouped send/recv through the transport
+ *     (NCCL or the in-process world) between separate kernels.
+ * FMOE_F64 / FMOE_F32 layers always use the transport.  Set before the
+ * first forward, identically on every rank. */
+/* Host arithmetic of the fused exchange (pure, no device): from the
+ * all-gathered counts [world][world*local_experts] (rows rank s routes to
+ * global expert g, as exchange_counts delivers them, collectives.cpp:69-109),
+ * rank `rank`'s layouts (as fmoe_ep_layout) plus
+ *   g_rank[g], g_delta[g]: its send rows of expert g land in rank g_rank[g]'s
+ *     receive layout at (send position + g_delta[g]);
+ *   route[3][local_experts*world]: for receive chunk c = e*world + s, its first
+ *     row, its row count and its first row in rank s's send layout. */
+int fmoe_ep_routes(int world, int rank, int64_t local_experts, int64_t align, const int64_t* counts,
+                   int64_t* send_off, int64_t* chunk_off, int64_t* block_off, int64_t* rows, int32_t* g_rank,
+                   int64_t* g_delta, int32_t* route);
+#define FMOE_EP_EXCHANGE_PEER 0
+#define FMOE_EP_EXCHANGE_TRANSPORT 1
+int fmoe_layer_set_ep_exchange(fmoe_layer* layer, int mode);
+/* *fused = 1 when the last forward ran the fused peer-memory exchange. */
+int fmoe_layer_ep_exchange_fused(fmoe_layer* layer, int* fused);
 
 /* ExchangePlan (collectives.hpp:16-33), host arrays of world*local_experts
  * entries owned by the caller: send_counts[dest][local expert],

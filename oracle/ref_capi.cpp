@@ -434,6 +434,64 @@ int ref_bench_step(void* handle) {
 
 void ref_bench_destroy(void* handle) { delete static_cast<RefBench*>(handle); }
 
+// Injected-routing CPU baseline: the reference's dispatch +
+// expert pool with a given IndexMatrix and scores instead of its gate --
+// build_plan -> scatter -> multi_expert_forward -> gather_combine, then
+// gather_combine_backward -> multi_expert_backward -> scatter_backward
+// (dispatch.cpp:10-126, expert.cpp:85-125).
+struct RefRoutedBench {
+  MoELayerState st;
+  Matrix x, dy, scores;
+  IndexMatrix idx;
+};
+
+void* ref_bench_routed_create(uint64_t seed, int64_t n, int64_t d, int64_t h, int64_t e, int64_t k,
+                              const int64_t* idx, const double* scores) {
+  try {
+    MoEConfig cfg;
+    cfg.n_b = static_cast<std::size_t>(n);
+    cfg.d_m = static_cast<std::size_t>(d);
+    cfg.d_h = static_cast<std::size_t>(h);
+    cfg.k = static_cast<std::size_t>(k);
+    cfg.n_e_local = static_cast<std::size_t>(e);
+    cfg.world_size = 1;
+    cfg.seed = seed;
+    auto* b = new RefRoutedBench;
+    b->st = init_state(cfg, 0);
+    b->x = Matrix(static_cast<std::size_t>(n), static_cast<std::size_t>(d));
+    b->dy = Matrix(static_cast<std::size_t>(n), static_cast<std::size_t>(d));
+    UniformRng(stream_seed(seed, 102)).fill(b->x, -1.0, 1.0);
+    UniformRng(stream_seed(seed, 103)).fill(b->dy, -1.0, 1.0);
+    b->idx = IndexMatrix(static_cast<std::size_t>(n), static_cast<std::size_t>(k));
+    b->scores = Matrix(static_cast<std::size_t>(n), static_cast<std::size_t>(k));
+    for (int64_t i = 0; i < n * k; ++i) {
+      b->idx.data()[i] = idx[i];
+      b->scores.data()[i] = scores[i];
+    }
+    return b;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return nullptr;
+  }
+}
+
+int ref_bench_routed_step(void* handle) {
+  return guarded([&] {
+    auto* b = static_cast<RefRoutedBench*>(handle);
+    const DispatchPlan plan = build_plan(b->idx, b->st.experts.size());
+    const Matrix xs = scatter(b->x, plan);
+    MultiExpertResult fwd = multi_expert_forward(xs, plan.counts, b->st.experts);
+    const Matrix y = gather_combine(fwd.ys, plan, b->scores);
+    GatherCombineGrads g = gather_combine_backward(b->dy, fwd.ys, plan, b->scores);
+    MultiExpertGrads eg = multi_expert_backward(g.d_ys, fwd.caches, b->st.experts);
+    const Matrix dx = scatter_backward(eg.d_xs, plan);
+    (void)y;
+    (void)dx;
+  });
+}
+
+void ref_bench_routed_destroy(void* handle) { delete static_cast<RefRoutedBench*>(handle); }
+
 // exchange_counts over an InProcWorld: local_counts [world][E_total] in,
 // recv_counts [world][world*e_local] out (collectives.cpp:69-109).
 int ref_exchange_counts(const int64_t* local_counts, int64_t world, int64_t total,

@@ -35,6 +35,7 @@ from .api import (  # noqa: F401
     all_to_all_rows,
     all_to_all_rows_reverse,
     ep_layout,
+    ep_routes,
     allreduce_sum,
     matmul,
     softmax_rows,

@@ -79,6 +79,8 @@ EXPORTS = [
     "fmoe_ctx_join_world", "fmoe_exchange_counts", "fmoe_ep_layout", "fmoe_a2a_rows",
     "fmoe_a2a_rows_reverse", "fmoe_allreduce_sum", "fmoe_matmul", "fmoe_softmax_rows", "fmoe_topk_rows",
     "fmoe_experts_fwd_cached", "fmoe_experts_bwd_cached", "fmoe_layer_train_step", "fmoe_layer_sync_masters",
+    "fmoe_layer_fwd_routed", "fmoe_layer_routing_grad", "fmoe_layer_set_ep_exchange",
+    "fmoe_layer_ep_exchange_fused", "fmoe_ep_routes",
 ]
 
 
@@ -123,6 +125,11 @@ def _load():
         "fmoe_layer_routing": [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(Plan)],
         "fmoe_layer_fwd": [vp, vp, vp],
         "fmoe_layer_bwd": [vp, vp, vp],
+        "fmoe_layer_fwd_routed": [vp, vp, vp, vp, vp],
+        "fmoe_layer_routing_grad": [vp, C.POINTER(vp)],
+        "fmoe_layer_set_ep_exchange": [vp, C.c_int],
+        "fmoe_ep_routes": [C.c_int, C.c_int, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp],
+        "fmoe_layer_ep_exchange_fused": [vp, C.POINTER(C.c_int)],
         "fmoe_world_create": [C.c_int, C.POINTER(vp)],
         "fmoe_world_destroy": [vp],
         "fmoe_ctx_join_world": [vp, vp, C.c_int],

@@ -201,6 +201,26 @@ def ep_layout(world: int, local_experts: int, align: int, send_counts, recv_coun
     return so, co.reshape(local_experts, world), bo, rows
 
 
+def ep_routes(world: int, rank: int, local_experts: int, align: int, counts):
+    """Host arithmetic of the fused peer-memory exchange (fmoe_ep_routes) from
+    the all-gathered counts [world, world*local_experts]: (send_off, chunk_off
+    [el, W], block_off, rows, g_rank [E], g_delta [E], route [3, el, W])."""
+    import numpy as np
+
+    e = world * local_experts
+    c = np.ascontiguousarray(np.asarray(counts, np.int64).reshape(world, e))
+    so = np.zeros(e, np.int64)
+    co = np.zeros(e, np.int64)
+    bo = np.zeros(local_experts + 1, np.int64)
+    rows = np.zeros(local_experts, np.int64)
+    gr = np.zeros(e, np.int32)
+    gd = np.zeros(e, np.int64)
+    rt = np.zeros(3 * e, np.int32)
+    check(lib.fmoe_ep_routes(world, rank, local_experts, align, c.ctypes.data, so.ctypes.data, co.ctypes.data,
+                             bo.ctypes.data, rows.ctypes.data, gr.ctypes.data, gd.ctypes.data, rt.ctypes.data))
+    return so, co.reshape(local_experts, world), bo, rows, gr, gd, rt.reshape(3, local_experts, world)
+
+
 def _ctx(t: torch.Tensor) -> Context:
     return Context.get(t.device)
 
@@ -518,6 +538,23 @@ class MoELayer:
         """Expert parallelism inside one process (one host thread per rank)."""
         self.ctx.join_world(world, self.rank)
 
+    def set_ep_exchange(self, mode: str):
+        """'peer' (default): the expert-parallel row exchanges are fused into
+        the scatter / expert-GEMM epilogues over NVLink peer memory;
+        'transport': grouped send/recv through the transport.  Before the
+        first forward, identically on every rank."""
+        code = {"peer": 0, "transport": 1}.get(mode)
+        if code is None:
+            raise ShapeError(f"set_ep_exchange: unknown mode {mode!r}")
+        check(lib.fmoe_layer_set_ep_exchange(self.h, code))
+
+    @property
+    def ep_exchange_fused(self) -> bool:
+        """True when the last forward ran the fused peer-memory exchange."""
+        v = C.c_int()
+        check(lib.fmoe_layer_ep_exchange_fused(self.h, C.byref(v)))
+        return bool(v.value)
+
     def _views(self):
         c = self.config
         e, el, d, hh = c.total_experts(), c.n_e_local, c.d_m, c.d_h
@@ -563,6 +600,37 @@ class MoELayer:
         check(lib.fmoe_layer_fwd(self.h, _p(x), _p(y)))
         self._x = x
         return y
+
+    def forward_routed(self, x: torch.Tensor, topk_idx: torch.Tensor, topk_scores: torch.Tensor,
+                       y: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """forward with injected routing (the reference's build_plan fed a
+        sampled IndexMatrix, dispatch.hpp:28): no gate.
+        topk_idx [n_b, k] int32, topk_scores [n_b, k] in the score dtype.  The
+        next backward() returns d_x = scatter_backward(d_xs) and leaves
+        d(topk_scores) in routing_grad()."""
+        x = _dev(x)
+        c = self.config
+        if x.shape != (c.n_b, c.d_m) or x.dtype != self.dtype:
+            raise ShapeError(f"forward_routed: expected x [{c.n_b}, {c.d_m}] {self.dtype}")
+        idx = _dev(topk_idx)
+        sc = _dev(topk_scores)
+        if idx.shape != (c.n_b, c.k) or idx.dtype != torch.int32:
+            raise ShapeError(f"forward_routed: expected topk_idx [{c.n_b}, {c.k}] int32")
+        if sc.shape != (c.n_b, c.k) or sc.dtype != score_dtype(self.dtype):
+            raise ShapeError(f"forward_routed: expected topk_scores [{c.n_b}, {c.k}] {score_dtype(self.dtype)}")
+        if y is None:
+            y = torch.empty_like(x)
+        self.ctx.use_current_stream()
+        check(lib.fmoe_layer_fwd_routed(self.h, _p(x), _p(idx), _p(sc), _p(y)))
+        self._x, self._routing_in = x, (idx, sc)
+        return y
+
+    def routing_grad(self) -> torch.Tensor:
+        """d(topk_scores) [n_b, k] of the last backward (gather_combine_backward's d_w)."""
+        c = self.config
+        p = C.c_void_p()
+        check(lib.fmoe_layer_routing_grad(self.h, C.byref(p)))
+        return _wrap(p.value, (c.n_b, c.k), score_dtype(self.dtype), self.device, self)
 
     def backward(self, dy: torch.Tensor, dx: Optional[torch.Tensor] = None) -> torch.Tensor:
         """backward (moe_layer.cpp:112-142): returns d_x; parameter gradients

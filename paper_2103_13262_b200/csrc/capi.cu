@@ -85,6 +85,10 @@ int fmoe_ctx_destroy(fmoe_ctx* ctx) {
     Ctx* c = C(ctx);
     cudaFree(c->d_error);
     if (c->ws) cudaFree(c->ws);
+    if (c->copy_in) cudaStreamDestroy(c->copy_in);
+    if (c->copy_out) cudaStreamDestroy(c->copy_out);
+    for (auto e : c->ev_io)
+      if (e) cudaEventDestroy(e);
     delete c;
   })
 }
@@ -110,6 +114,8 @@ int fmoe_ctx_profile(fmoe_ctx* ctx, int n_steps) {
       auto* p = new Prof;
       p->steps = n_steps;
       p->ev.resize((size_t)n_steps * N_MARKS);
+      p->prev.assign((size_t)n_steps * N_MARKS, (int8_t)-1);
+      p->last.assign((size_t)n_steps, (int8_t)-1);
       for (auto& e : p->ev) CK(cudaEventCreate(&e));
       c->prof = p;
     }
@@ -123,13 +129,15 @@ int fmoe_ctx_profile_read(fmoe_ctx* ctx, float* stage_ms, int n_stages, int* ste
     if (!p) shape_error("profiling not armed");
     CK(cudaStreamSynchronize(c->stream));
     for (int i = 0; i < n_stages; ++i) stage_ms[i] = 0.f;
-    for (int s = 0; s < p->step; ++s)
+    for (int s = 0; s < p->used; ++s)
       for (int i = 1; i < N_MARKS && i < n_stages; ++i) {
+        const int from = p->prev[(size_t)s * N_MARKS + i];
+        if (from < 0) continue;
         float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, p->ev[(size_t)s * N_MARKS + i - 1], p->ev[(size_t)s * N_MARKS + i]));
+        CK(cudaEventElapsedTime(&ms, p->ev[(size_t)s * N_MARKS + from], p->ev[(size_t)s * N_MARKS + i]));
         stage_ms[i] += ms;
       }
-    if (steps_done) *steps_done = p->step;
+    if (steps_done) *steps_done = p->used;
   })
 }
 

@@ -22,6 +22,7 @@ LocalWorld::~LocalWorld() {
   for (auto& s : slots) {
     cudaEventDestroy(s.ready);
     cudaEventDestroy(s.done);
+    for (auto e : s.phase) cudaEventDestroy(e);
   }
 }
 
@@ -47,6 +48,7 @@ struct LocalTransport : Transport {
     rank = r;
     world = lw->world;
   }
+  LocalWorld* local_world() override { return w; }
   void group(Ctx* ctx, const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs) override {
     auto& me = w->slots[rank];
     me.sends.clear();

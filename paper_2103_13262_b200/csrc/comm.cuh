@@ -37,6 +37,8 @@ struct Transport {
   // to b is matched with the i-th recv of b from a; sizes must agree
   // (ProtocolError otherwise).  Zero-byte entries are skipped on both sides.
   virtual void group(Ctx* ctx, const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs) = 0;
+  // The in-process world behind this transport (nullptr for NCCL).
+  virtual struct LocalWorld* local_world() { return nullptr; }
 };
 
 struct LocalWorld {
@@ -50,6 +52,7 @@ struct LocalWorld {
   struct Slot {
     std::vector<Xfer> sends;
     cudaEvent_t ready = nullptr, done = nullptr;
+    std::vector<cudaEvent_t> phase;  // peer-memory phase events of the rank (peer.cuh)
   };
   std::vector<Slot> slots;
   void barrier();

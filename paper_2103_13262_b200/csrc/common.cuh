@@ -45,9 +45,15 @@ enum Mark : int {
   MARK_BWD_BEGIN, MARK_GCB, MARK_DGRAD2, MARK_WGRAD2, MARK_DB2, MARK_DGRAD1, MARK_WGRAD1, MARK_DB1,
   MARK_GATE_DWG, MARK_GATE_DX, N_MARKS
 };
+// A stage's time runs from the mark recorded just before it in the same step
+// (the issue order differs between paths), so prev[] keeps that mark's id.
+// Each layer forward takes the next slot and its backward records into the
+// same slot, so stacks of layers sharing one context profile per layer-step.
 struct Prof {
-  std::vector<cudaEvent_t> ev;  // [steps][N_MARKS]
-  int steps = 0, step = 0;
+  std::vector<cudaEvent_t> ev;  // [slots][N_MARKS]
+  std::vector<int8_t> prev;     // [slots][N_MARKS]: preceding mark, -1 = not recorded
+  std::vector<int8_t> last;     // [slots]: last mark recorded in the slot
+  int steps = 0, used = 0;      // slots allocated / taken
 };
 
 struct Ctx {
@@ -62,13 +68,26 @@ struct Ctx {
   size_t ws_size = 0;
   int world = 1, rank = 0;
   Prof* prof = nullptr;
+  int prof_slot = -1;      // slot of the layer step being issued (-1: none)
+  // host-buffer steps (Layer::step_host): input / output copy engines run on
+  // their own streams so PCIe transfers overlap the layer's kernels
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  cudaEvent_t ev_io[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 
 inline void ctx_mark(Ctx* c, int id) {
   Prof* p = c->prof;
-  if (!p || p->step >= p->steps) return;
-  cudaEventRecord(p->ev[(size_t)p->step * N_MARKS + id], c->stream);
-  if (id == MARK_GATE_DX) p->step++;
+  if (!p || c->prof_slot < 0 || c->prof_slot >= p->used) return;
+  const size_t base = (size_t)c->prof_slot * N_MARKS;
+  cudaEventRecord(p->ev[base + id], c->stream);
+  p->prev[base + id] = p->last[c->prof_slot];
+  p->last[c->prof_slot] = (int8_t)id;
+}
+// A layer forward takes a new profiling slot (-1 when none is left).
+inline int ctx_take_slot(Ctx* c) {
+  Prof* p = c->prof;
+  c->prof_slot = (p && p->used < p->steps) ? p->used++ : -1;
+  return c->prof_slot;
 }
 
 // ------------------------------------------------------------- type traits

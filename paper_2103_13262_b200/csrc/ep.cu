@@ -13,6 +13,7 @@
 // The plan of the forward is reused by the backward without a recount
 // (collectives.hpp:48-50).  Chunks are exchanged per (peer, local expert)
 // straight into their final slots, so the receive side needs no permute.
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -20,6 +21,8 @@
 #include "comm.cuh"
 #include "layer.cuh"
 #include "ops.cuh"
+#include "peer.cuh"
+#include "plan.cuh"
 
 namespace fmoe_b200 {
 
@@ -34,6 +37,19 @@ struct Layer::Ep {
   // receive-space activations
   void *xs = nullptr, *hidden = nullptr, *ys = nullptr, *d_ys = nullptr, *d_pre = nullptr, *d_xs = nullptr;
   bool planned = false;
+  // fused exchange over NVLink peer memory (peer.cuh); bf16 only
+  int exchange = FMOE_EP_EXCHANGE_PEER;  // or FMOE_EP_EXCHANGE_TRANSPORT
+  PeerSet peer;
+  bool peer_tried = false;
+  int32_t* cnt_mat = nullptr;   // [W][E] all-gathered send counts (peer-written)
+  uint32_t* flags = nullptr;    // [PH_N][W] epoch flags (peer-written)
+  int32_t* g_rank = nullptr;    // [E] destination rank of global expert g
+  int64_t* g_delta = nullptr;   // [E] row shift send layout -> destination receive layout
+  int32_t* rt = nullptr;        // [3][el*W] chunk start / rows / destination row (RowRoute)
+  uint8_t* h_peer = nullptr;    // pinned staging of the tables above
+  void* peer_scratch = nullptr; // connect's blob exchange
+  void** peer_table = nullptr;  // [PB_N][W] device pointer tables
+  bool fused = false;           // the current step runs the fused path
 };
 
 namespace {
@@ -51,7 +67,8 @@ void Layer::ep_alloc() {
   P.W = (int)cfg.world_size;
   P.r = (int)cfg.rank;
   P.el = cfg.n_e_local;
-  P.align = t == FMOE_BF16 ? 256 : 1;  // CTA-pair GEMM tiles
+  // a rank's experts receive n_b*k rows on average (its own token count)
+  P.align = t == FMOE_BF16 ? expert_block_align(cfg.n_b * cfg.k, P.el) : 1;
   // worst case: every token of every rank picks this rank's experts
   P.cap_recv = plan_capacity(cfg.n_b * cfg.world_size, cfg.k, P.el, P.align);
   const int64_t d = cfg.d_m, h = cfg.d_h, cap = P.cap_recv;
@@ -76,6 +93,16 @@ void Layer::ep_alloc() {
   P.d_xs = alloc(owned, cap * d * es);
   tpart = (float*)alloc(owned, experts_bwd_part_floats(P.rplan, d, h) * 4);
   if (t == FMOE_BF16) relu_bits = (uint32_t*)alloc(owned, cap * (h / 32) * 4);
+  const int64_t W = P.W;
+  P.cnt_mat = (int32_t*)alloc(owned, W * E * 4);
+  P.flags = (uint32_t*)alloc(owned, PH_N * W * 4);
+  CK(cudaMemset(P.flags, 0, PH_N * W * 4));
+  P.g_rank = (int32_t*)alloc(owned, E * 4);
+  P.g_delta = (int64_t*)alloc(owned, E * 8);
+  P.rt = (int32_t*)alloc(owned, 3 * P.el * W * 4);
+  CK(cudaMallocHost(&P.h_peer, W * E * 4 + E * 12 + 3 * P.el * W * 4 + 64));
+  P.peer_scratch = alloc(owned, (int64_t)PeerSet::scratch_bytes(P.W));
+  P.peer_table = (void**)alloc(owned, PB_N * W * (int64_t)sizeof(void*));
 }
 
 namespace {
@@ -167,6 +194,49 @@ void ep_layout(int W, int64_t el, int64_t align, const int64_t* send, const int6
   block_off[el] = at;
 }
 
+// Every rank's layout from the all-gathered count matrix counts[s][g] (rows
+// rank s routes to global expert g), as seen by rank r (pure host arithmetic,
+// exported as fmoe_ep_routes for the CPU tests):
+//   send_off/chunk_off/block_off/rows  rank r's own layouts (ep_layout)
+//   g_rank[g], g_delta[g]   my send rows of expert g -> rank g/el's receive
+//                           buffer at row (send position + g_delta[g])
+//   route[c], route[C + c], route[2C + c]  (c = e*W + s, C = el*W): my receive
+//                           chunk (local expert e, source s) -- first row, row
+//                           count -- and its first row in s's send layout
+void ep_routes(int W, int r, int64_t el, int64_t align, const int64_t* counts, int64_t* send_off,
+               int64_t* chunk_off, int64_t* block_off, int64_t* rows, int32_t* g_rank, int64_t* g_delta,
+               int32_t* route) {
+  const int64_t E = (int64_t)W * el, C = el * W;
+  std::vector<std::vector<int64_t>> so(W), co(W);
+  std::vector<int64_t> rcv(E), blk(el + 1), rw(el);
+  for (int p = 0; p < W; ++p) {
+    for (int s = 0; s < W; ++s)
+      for (int64_t e = 0; e < el; ++e) rcv[s * el + e] = counts[(int64_t)s * E + p * el + e];
+    so[p].assign(E, 0);
+    co[p].assign(C, 0);
+    ep_layout(W, el, align, counts + (int64_t)p * E, rcv.data(), so[p].data(), co[p].data(), blk.data(),
+              rw.data());
+    if (p == r) {
+      std::copy(so[p].begin(), so[p].end(), send_off);
+      std::copy(co[p].begin(), co[p].end(), chunk_off);
+      std::copy(blk.begin(), blk.end(), block_off);
+      std::copy(rw.begin(), rw.end(), rows);
+    }
+  }
+  for (int64_t g = 0; g < E; ++g) {
+    const int p = (int)(g / el);
+    g_rank[g] = p;
+    g_delta[g] = co[p][(g % el) * W + r] - so[r][g];
+  }
+  for (int64_t e = 0; e < el; ++e)
+    for (int s = 0; s < W; ++s) {
+      const int64_t c = e * W + s;
+      route[c] = (int32_t)co[r][c];
+      route[C + c] = (int32_t)counts[(int64_t)s * E + r * el + e];
+      route[2 * C + c] = (int32_t)so[s][r * el + e];
+    }
+}
+
 // exchange_counts (collectives.cpp:69-109) + the receive layout
 // (recv_chunk_offsets, collectives.cpp:126-135) with aligned expert blocks.
 static void ep_plan(Layer& L, Transport* tr) {
@@ -217,6 +287,73 @@ static void ep_plan(Layer& L, Transport* tr) {
   P.planned = true;
 }
 
+// ------------------------------------------------ fused exchange (peer memory)
+// Connect the peer buffers on the first bf16 EP step (collective: every rank
+// runs its first forward together).  Ranks that cannot map each other (no
+// NVLink P2P / different hosts) all keep the transport exchange.
+static bool ep_use_peer(Layer& L, Transport* tr) {
+  Layer::Ep& P = *L.ep;
+  if (L.t != FMOE_BF16 || P.exchange != FMOE_EP_EXCHANGE_PEER) return false;
+  if (!P.peer_tried) {
+    P.peer_tried = true;
+    void* bufs[PB_N] = {P.xs, P.d_ys, L.ys, L.d_xs, P.cnt_mat, P.flags};
+    P.peer.connect(L.ctx, tr, bufs, P.peer_scratch, P.peer_table);
+  }
+  return P.peer.ok;
+}
+
+// Count all-gather over peer memory (exchange_counts, collectives.cpp:69-109:
+// every rank receives every rank's full count vector), the one host sync of
+// an EP step, then the layouts of ALL ranks: this rank's receive layout (as
+// ep_plan), where each of its send chunks lands in the destination's receive
+// layout (scatter / gather-combine-backward routes) and where each received
+// chunk goes home (fc2 / dgrad-fc1 epilogue routes).
+static void ep_plan_peer(Layer& L) {
+  Ctx* ctx = L.ctx;
+  Layer::Ep& P = *L.ep;
+  const int W = P.W, r = P.r;
+  const int64_t el = P.el, E = L.E;
+  P.peer.put_counts(ctx, L.plan.counts, E);
+  P.peer.wait(ctx, PH_COUNTS);
+  int32_t* hc = reinterpret_cast<int32_t*>(P.h_peer);
+  CK(cudaMemcpyAsync(hc, P.cnt_mat, W * E * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));  // the one host sync of an EP step
+  std::vector<int64_t> cnt(hc, hc + W * E);
+  int32_t* grank = hc + W * E;
+  int64_t* gdelta = reinterpret_cast<int64_t*>(P.h_peer + ((W * E * 4 + E * 4 + 7) & ~int64_t(7)));
+  int32_t* rt = reinterpret_cast<int32_t*>(gdelta + E);
+  P.send_off.assign(E, 0);
+  P.chunk_off.assign(el * W, 0);
+  P.block_off.assign(el + 1, 0);
+  P.rows.assign(el, 0);
+  ep_routes(W, r, el, P.align, cnt.data(), P.send_off.data(), P.chunk_off.data(), P.block_off.data(),
+            P.rows.data(), grank, gdelta, rt);
+  P.h_send.assign(cnt.begin() + (int64_t)r * E, cnt.begin() + (int64_t)(r + 1) * E);
+  P.h_recv.assign((size_t)W * el, 0);
+  for (int s = 0; s < W; ++s)
+    for (int64_t e = 0; e < el; ++e) P.h_recv[s * el + e] = cnt[(int64_t)s * E + r * el + e];
+  if (P.block_off[el] > P.cap_recv) protocol_error("exchange: received rows exceed the layer capacity");
+  CK(cudaMemcpyAsync(P.g_rank, grank, E * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(P.g_delta, gdelta, E * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(P.rt, rt, 3 * el * W * 4, cudaMemcpyHostToDevice, ctx->stream));
+  // receive block plan (counts, offsets, 128-row tile table), as ep_plan
+  int32_t* up = P.h_pinned + E + W * el;
+  for (int64_t e = 0; e < el; ++e) up[e] = (int32_t)P.rows[e];
+  int32_t* uo = up + el;
+  for (int64_t e = 0; e <= el; ++e) uo[e] = (int32_t)P.block_off[e];
+  int32_t* ut = uo + el + 1;
+  int64_t nt = 0;
+  for (int64_t e = 0; e < el; ++e)
+    for (int64_t tt = P.block_off[e] / 128; tt < P.block_off[e + 1] / 128; ++tt) ut[nt++] = (int32_t)e;
+  ut[nt] = (int32_t)nt;
+  CK(cudaMemcpyAsync(P.rplan.counts, up, el * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(P.rplan.offsets, uo, (el + 1) * 4, cudaMemcpyHostToDevice, ctx->stream));
+  if (nt) CK(cudaMemcpyAsync(P.rplan.tile_expert, ut, nt * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(P.rplan.n_tiles, ut + nt, 4, cudaMemcpyHostToDevice, ctx->stream));
+  // the staging is reused next step only after this step's host sync
+  P.planned = true;
+}
+
 void Layer::ep_check() const { need_transport(ctx, cfg); }
 
 void Layer::ep_forward(const void* x, void* y) {
@@ -225,6 +362,28 @@ void Layer::ep_forward(const void* x, void* y) {
   const int64_t d = cfg.d_m, h = cfg.d_h;
   const size_t rb = (size_t)d * es;
   plan_build(ctx, idx, plan);                  // send plan over all E experts, reference layout
+  P.fused = ep_use_peer(*this, tr);
+  if (P.fused) {
+    // fused: scatter straight into the expert ranks (global_scatter), fc2
+    // epilogue straight back into the source ranks (global_gather)
+    P.peer.epoch++;
+    ep_plan_peer(*this);                       // C1 + every rank's layout
+    ctx_mark(ctx, MARK_PLAN);
+    zero_pads(ctx, P, rb, P.xs);
+    ScatterRoute sr{idx, P.g_rank, P.g_delta, P.peer.d_ptr[PB_XS]};
+    scatter(ctx, t, x, d, plan, nullptr, &sr);  // C2 fused
+    P.peer.signal(ctx, PH_SCATTER);
+    P.peer.wait(ctx, PH_SCATTER);
+    ctx_mark(ctx, MARK_SCATTER);
+    const int64_t c = P.el * P.W;
+    RowRoute rr{P.peer.d_ptr[PB_YS], P.rt, P.rt + c, P.rt + 2 * c, P.W};
+    experts_fwd(ctx, t, P.rplan, d, h, params(), P.xs, P.hidden, P.ys, relu_bits, nullptr, &rr);  // C3 fused
+    P.peer.signal(ctx, PH_GATHER);
+    P.peer.wait(ctx, PH_GATHER);
+    gather_combine(ctx, t, ys, d, plan, vals, y);
+    ctx_mark(ctx, MARK_GATHER);
+    return;
+  }
   scatter(ctx, t, x, d, plan, xs);
   ep_plan(*this, tr);                          // C1 + receive layout
   ctx_mark(ctx, MARK_PLAN);
@@ -243,17 +402,52 @@ void Layer::ep_backward(const void* dy, void* dx) {
   if (!P.planned) protocol_error("backward: no expert-parallel forward cache");
   const int64_t n = cfg.n_b, d = cfg.d_m, h = cfg.d_h, k = cfg.k;
   const size_t rb = (size_t)d * es;
-  const bool bf = t == FMOE_BF16;
+  const bool bf = t == FMOE_BF16, gate = bf && !routed;
   ctx_mark(ctx, MARK_BWD_BEGIN);
-  gather_combine_bwd(ctx, t, dy, ys, d, plan, vals, d_ys, d_w, bf ? scores : nullptr, bf ? idx : nullptr,
-                     bf ? dz_bf16 : nullptr);
+  if (P.fused) {
+    // gradients ride the same routes: d_ys straight into the expert ranks,
+    // the dgrad-fc1 epilogue straight back into the source ranks; the weight
+    // gradients and the gate's d_wg run while the peers finish
+    zero_pads(ctx, P, rb, P.d_ys);
+    ScatterRoute sr{idx, P.g_rank, P.g_delta, P.peer.d_ptr[PB_DYS]};
+    gather_combine_bwd(ctx, t, dy, ys, d, plan, vals, nullptr, d_w, gate ? scores : nullptr,
+                       gate ? idx : nullptr, gate ? dz_bf16 : nullptr, &sr);
+    P.peer.signal(ctx, PH_SCATTER_BWD);
+    P.peer.wait(ctx, PH_SCATTER_BWD);
+    ctx_mark(ctx, MARK_GCB);
+    const int64_t c = P.el * P.W;
+    RowRoute rr{P.peer.d_ptr[PB_DXS], P.rt, P.rt + c, P.rt + 2 * c, P.W};
+    experts_bwd(ctx, t, P.rplan, d, h, params(), P.xs, P.hidden, P.d_ys, P.d_xs, grads(), P.d_pre, tpart,
+                relu_bits, nullptr, EXPERTS_BWD_DGRAD, &rr);
+    P.peer.signal(ctx, PH_GATHER_BWD);
+    experts_bwd(ctx, t, P.rplan, d, h, params(), P.xs, P.hidden, P.d_ys, P.d_xs, grads(), P.d_pre, tpart,
+                relu_bits, nullptr, EXPERTS_BWD_WGRAD);
+    if (routed) {
+      CK(cudaMemsetAsync(dwg, 0, (size_t)d * E * ss, ctx->stream));
+      P.peer.wait(ctx, PH_GATHER_BWD);
+      scatter_bwd(ctx, t, d_xs, d, plan, dx, nullptr);
+    } else {
+      gate_dwg_bf16(ctx, x_saved, dz_bf16, n, d, E, part, (float*)dwg);
+      ctx_mark(ctx, MARK_GATE_DWG);
+      gate_dx_bf16(ctx, dz_bf16, wg, n, d, E, nullptr, nullptr, 0, gdx);
+      P.peer.wait(ctx, PH_GATHER_BWD);
+      scatter_bwd(ctx, t, d_xs, d, plan, dx, gdx);
+    }
+    ctx_mark(ctx, MARK_GATE_DX);
+    return;
+  }
+  gather_combine_bwd(ctx, t, dy, ys, d, plan, vals, d_ys, d_w, gate ? scores : nullptr, gate ? idx : nullptr,
+                     gate ? dz_bf16 : nullptr);
   zero_pads(ctx, P, rb, P.d_ys);
   exchange_rows(ctx, tr, P, rb, d_ys, P.d_ys, true);  // gradients ride the same routes
   ctx_mark(ctx, MARK_GCB);
   experts_bwd(ctx, t, P.rplan, d, h, params(), P.xs, P.hidden, P.d_ys, P.d_xs, grads(), P.d_pre, tpart,
               relu_bits);
   exchange_rows(ctx, tr, P, rb, P.d_xs, d_xs, false);
-  if (bf) {
+  if (routed) {  // injected routing: no gate, d_x is scatter_backward alone
+    CK(cudaMemsetAsync(dwg, 0, (size_t)d * E * ss, ctx->stream));
+    scatter_bwd(ctx, t, d_xs, d, plan, dx, nullptr);
+  } else if (bf) {
     gate_dwg_bf16(ctx, x_saved, dz_bf16, n, d, E, part, (float*)dwg);
     ctx_mark(ctx, MARK_GATE_DWG);
     gate_dx_bf16(ctx, dz_bf16, wg, n, d, E, nullptr, nullptr, 0, gdx);
@@ -269,7 +463,12 @@ void Layer::ep_backward(const void* dy, void* dx) {
 }  // namespace fmoe_b200
 
 namespace fmoe_b200 {
-void Layer::ep_free(Ep* e) { delete e; }
+void Layer::ep_free(Ep* e) {
+  if (!e) return;
+  e->peer.close();
+  if (e->h_peer) cudaFreeHost(e->h_peer);
+  delete e;
+}
 }  // namespace fmoe_b200
 
 // ------------------------------------------------------------------- C-ABI
@@ -414,6 +613,39 @@ void a2a(Ctx* c, fmoe_dtype dt, const void* src, int64_t d, const fmoe_exchange_
 }  // namespace
 
 extern "C" {
+
+int fmoe_ep_routes(int world, int rank, int64_t local_experts, int64_t align, const int64_t* counts,
+                   int64_t* send_off, int64_t* chunk_off, int64_t* block_off, int64_t* rows, int32_t* g_rank,
+                   int64_t* g_delta, int32_t* route) {
+  FMOE_GUARD({
+    if (world < 1 || rank < 0 || rank >= world || local_experts < 1 || align < 1) shape_error("ep_routes: bad sizes");
+    if (!counts || !send_off || !chunk_off || !block_off || !rows || !g_rank || !g_delta || !route)
+      shape_error("ep_routes: null buffer");
+    ep_routes(world, rank, local_experts, align, counts, send_off, chunk_off, block_off, rows, g_rank, g_delta,
+              route);
+  })
+}
+
+int fmoe_layer_set_ep_exchange(fmoe_layer* layer, int mode) {
+  FMOE_GUARD({
+    if (!layer) shape_error("null layer");
+    if (mode != FMOE_EP_EXCHANGE_PEER && mode != FMOE_EP_EXCHANGE_TRANSPORT)
+      shape_error("set_ep_exchange: unknown mode");
+    Layer* l = reinterpret_cast<Layer*>(layer);
+    if (l->ep) {
+      if (l->ep->peer_tried) protocol_error("set_ep_exchange: must be set before the first forward");
+      l->ep->exchange = mode;
+    }
+  })
+}
+
+int fmoe_layer_ep_exchange_fused(fmoe_layer* layer, int* fused) {
+  FMOE_GUARD({
+    if (!layer || !fused) shape_error("null argument");
+    Layer* l = reinterpret_cast<Layer*>(layer);
+    *fused = (l->ep && l->ep->fused) ? 1 : 0;
+  })
+}
 
 int fmoe_ep_layout(int world, int64_t local_experts, int64_t align, const int64_t* send_counts,
                    const int64_t* recv_counts, int64_t* send_off, int64_t* chunk_off, int64_t* block_off,

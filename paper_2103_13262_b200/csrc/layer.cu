@@ -8,10 +8,11 @@
 // FMOE_BF16 (product path), per step:
 //   fwd: gate GEMM+softmax+top-k (tcgen05) | plan x3 | scatter | fc1 (tcgen05,
 //        bias+relu) | fc2 (tcgen05, bias) | gather_combine
-//   bwd: gather_combine_bwd + gate Jacobian | dgrad fc2 (relu mask) | wgrad fc2 |
-//        db2 | dgrad fc1 | wgrad fc1 | db1 | gate dWg (split-K) + reduce |
-//        gate dx fused with scatter_backward
+//   bwd: gather_combine_bwd + gate Jacobian | dgrad fc2 (relu mask, d_b1
+//        partials) | dgrad fc1 | gate dx | scatter_backward  [d_x final] |
+//        wgrad fc2 | db2 | wgrad fc1 | db1 | gate dWg (split-K) + reduce
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "init.h"
@@ -21,6 +22,11 @@
 namespace fmoe_b200 {
 
 namespace {
+__global__ void count_out_of_range(const int32_t* __restrict__ idx, int64_t n, int32_t E, int* bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && (unsigned)__ldg(idx + i) >= (unsigned)E) atomicAdd(bad, 1);
+}
+
 template <typename T>
 T* dalloc(std::vector<void*>& owned, int64_t n) {
   void* p = nullptr;
@@ -75,7 +81,9 @@ Layer::Layer(Ctx* c, const fmoe_layer_config& cf) : ctx(c), cfg(cf) {
   plan.k = k;
   plan.n_experts = E;
   const bool ep_mode = cfg.world_size > 1;  // EP: plan/xs/ys are the send layout
-  plan.align = (bf && !ep_mode) ? 256 : 1;  // 256: CTA-pair GEMM tiles
+  // bf16 expert blocks: 256-row aligned (CTA-pair GEMM tiles) when experts
+  // average >= 1024 rows, else 128 (single-CTA tiles waste less padding)
+  plan.align = (bf && !ep_mode) ? expert_block_align(n * k, E) : 1;
   plan.capacity = plan_capacity(n, k, E, plan.align);
   plan.counts = dalloc<int32_t>(owned, E);
   plan.offsets = dalloc<int32_t>(owned, E + 1);
@@ -143,14 +151,53 @@ void Layer::init_weights() {
 }
 
 void Layer::forward(const void* x, void* y) {
-  const int64_t n = cfg.n_b, d = cfg.d_m, h = cfg.d_h, k = cfg.k;
+  const int64_t n = cfg.n_b, d = cfg.d_m, k = cfg.k;
   // moe_layer.cpp:70-75: validate the transport before any work is issued
   if (cfg.world_size > 1) ep_check();
   x_saved = x;
   fwd_done = false;
+  routed = false;
+  prof_slot = ctx_take_slot(ctx);
   ctx_mark(ctx, MARK_FWD_BEGIN);
   gate_fwd(ctx, t, x, wg, n, d, E, k, scores, idx, vals, logits);  // gate.cpp:23-35
   ctx_mark(ctx, MARK_GATE);
+  dispatch_and_experts(x, y);
+}
+
+// Injected routing (the reference feeds a sampled
+// IndexMatrix straight into build_plan, dispatch.hpp:28): the gate is skipped,
+// topk_idx [n_b, k] int32 / topk_scores [n_b, k] (score dtype) drive the same
+// plan -> scatter -> experts -> gather_combine; backward then yields d_x from
+// scatter_backward alone and d(topk_scores) (routing_grad), no gate gradients.
+void Layer::forward_routed(const void* x, const int32_t* topk_idx, const void* topk_scores, void* y) {
+  const int64_t n = cfg.n_b, k = cfg.k;
+  if (cfg.world_size > 1) ep_check();
+  x_saved = x;
+  fwd_done = false;
+  routed = true;
+  // build_plan validates before any work (dispatch.cpp:21-23): injected
+  // indices are checked here, synchronously, so a bad IndexMatrix throws
+  // ShapeError from this call and no kernel ever sees it
+  if (n * k > 0) {
+    CK(cudaMemsetAsync(ctx->d_error, 0, sizeof(int), ctx->stream));
+    count_out_of_range<<<(unsigned)ceil_div(n * k, 256), 256, 0, ctx->stream>>>(topk_idx, n * k, (int32_t)E,
+                                                                                ctx->d_error);
+    CK_LAUNCH(ctx);
+    int bad = 0;
+    CK(cudaMemcpyAsync(&bad, ctx->d_error, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (bad) shape_error("build_plan: expert index out of range (" + std::to_string(bad) + " entries)");
+  }
+  prof_slot = ctx_take_slot(ctx);
+  ctx_mark(ctx, MARK_FWD_BEGIN);
+  CK(cudaMemcpyAsync(idx, topk_idx, (size_t)n * k * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(vals, topk_scores, (size_t)n * k * ss, cudaMemcpyDeviceToDevice, ctx->stream));
+  ctx_mark(ctx, MARK_GATE);
+  dispatch_and_experts(x, y);
+}
+
+void Layer::dispatch_and_experts(const void* x, void* y) {
+  const int64_t d = cfg.d_m, h = cfg.d_h;
   if (cfg.world_size > 1) {
     ep_forward(x, y);
     fwd_done = true;
@@ -166,51 +213,101 @@ void Layer::forward(const void* x, void* y) {
   fwd_done = true;
 }
 
-void Layer::backward(const void* dy, void* dx) {
+void Layer::backward(const void* dy, void* dx, cudaEvent_t dx_ready) {
   if (!fwd_done) protocol_error("backward: no forward cache");
   const int64_t n = cfg.n_b, d = cfg.d_m, h = cfg.d_h, k = cfg.k;
+  ctx->prof_slot = prof_slot;  // the forward's profiling slot
   if (cfg.world_size > 1) {
     ep_backward(dy, dx);
+    if (dx_ready) CK(cudaEventRecord(dx_ready, ctx->stream));
+    ctx->prof_slot = -1;
     return;
   }
-  const bool bf = t == FMOE_BF16;
+  const bool bf = t == FMOE_BF16, gate = bf && !routed;
   ctx_mark(ctx, MARK_BWD_BEGIN);
   // dispatch.cpp:97-126 (+ gate.cpp:44-59 fused on the bf16 path)
-  gather_combine_bwd(ctx, t, dy, ys, d, plan, vals, d_ys, d_w, bf ? scores : nullptr, bf ? idx : nullptr,
-                     bf ? dz_bf16 : nullptr);
+  gather_combine_bwd(ctx, t, dy, ys, d, plan, vals, d_ys, d_w, gate ? scores : nullptr, gate ? idx : nullptr,
+                     gate ? dz_bf16 : nullptr);
   ctx_mark(ctx, MARK_GCB);
-  experts_bwd(ctx, t, plan, d, h, params(), xs, hidden, d_ys, d_xs, grads(), d_pre, tpart,
-              relu_bits);  // expert.cpp:104-125
-  if (bf) {
-    gate_dwg_bf16(ctx, x_saved, dz_bf16, n, d, E, part, (float*)dwg);                  // gate.cpp:62
-    ctx_mark(ctx, MARK_GATE_DWG);
-    // gate d_x on the tensor cores (gate.cpp:63, TMA-store epilogue), then
-    // scatter_backward adds it in the reference order (dispatch.cpp:80-95,
-    // moe_layer.cpp:140) as one HBM-bound pass
+  if (routed) {  // injected routing: no gate (see forward_routed), zero gate gradient
+    CK(cudaMemsetAsync(dwg, 0, (size_t)d * E * ss, ctx->stream));
+    const int ph = bf ? EXPERTS_BWD_DGRAD : EXPERTS_BWD_ALL;
+    experts_bwd(ctx, t, plan, d, h, params(), xs, hidden, d_ys, d_xs, grads(), d_pre, tpart, relu_bits,
+                nullptr, ph);
+    scatter_bwd(ctx, t, d_xs, d, plan, dx, nullptr);
+    ctx_mark(ctx, MARK_GATE_DX);
+    if (dx_ready) CK(cudaEventRecord(dx_ready, ctx->stream));
+    if (bf)
+      experts_bwd(ctx, t, plan, d, h, params(), xs, hidden, d_ys, d_xs, grads(), d_pre, tpart, relu_bits,
+                  nullptr, EXPERTS_BWD_WGRAD);
+  } else if (bf) {
+    // Data gradients first (expert.cpp:47-48,55), then the gate d_x on the
+    // tensor cores (gate.cpp:63, TMA-store epilogue) and scatter_backward
+    // adding it in the reference order (dispatch.cpp:80-95, moe_layer.cpp:140):
+    // d_x is final here and can leave the GPU while the weight gradients
+    // (expert.cpp:42-45,50-53; gate.cpp:62) are still being computed.
+    experts_bwd(ctx, t, plan, d, h, params(), xs, hidden, d_ys, d_xs, grads(), d_pre, tpart, relu_bits,
+                nullptr, EXPERTS_BWD_DGRAD);
     gate_dx_bf16(ctx, dz_bf16, wg, n, d, E, nullptr, nullptr, 0, gdx);
     scatter_bwd(ctx, t, d_xs, d, plan, dx, gdx);
+    ctx_mark(ctx, MARK_GATE_DX);
+    if (dx_ready) CK(cudaEventRecord(dx_ready, ctx->stream));
+    experts_bwd(ctx, t, plan, d, h, params(), xs, hidden, d_ys, d_xs, grads(), d_pre, tpart, relu_bits,
+                nullptr, EXPERTS_BWD_WGRAD);
+    gate_dwg_bf16(ctx, x_saved, dz_bf16, n, d, E, part, (float*)dwg);  // gate.cpp:62
+    ctx_mark(ctx, MARK_GATE_DWG);
   } else {
+    experts_bwd(ctx, t, plan, d, h, params(), xs, hidden, d_ys, d_xs, grads(), d_pre, tpart,
+                relu_bits);  // expert.cpp:104-125
     gate_bwd(ctx, t, x_saved, wg, scores, idx, d_w, n, d, E, k, dwg, gdx, dz, nullptr, nullptr);
     ctx_mark(ctx, MARK_GATE_DWG);
     scatter_bwd(ctx, t, d_xs, d, plan, dx, gdx);  // dispatch.cpp:80-95, moe_layer.cpp:140
+    ctx_mark(ctx, MARK_GATE_DX);
+    if (dx_ready) CK(cudaEventRecord(dx_ready, ctx->stream));
   }
-  ctx_mark(ctx, MARK_GATE_DX);
+  ctx->prof_slot = -1;
 }
 
+// One forward+backward on host buffers.  The PCIe copies run on the context's
+// two copy streams and overlap the kernels: d_y uploads while the forward
+// runs, y downloads during the backward, and d_x (final before the weight
+// gradients, see backward) downloads while they run.  x has nothing to hide
+// behind: every stage depends on the routing of all tokens.
 void Layer::step_host(const void* x_host, const void* dy_host, void* y_host, void* dx_host) {
   const int64_t nd = cfg.n_b * cfg.d_m;
   const size_t bytes = (size_t)nd * es;
   if (!io) {
     io = dalloc_bytes(owned, 4 * bytes);
   }
+  if (!ctx->copy_in) {
+    CK(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking));
+    for (auto& e : ctx->ev_io) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaEvent_t ev_x = ctx->ev_io[0], ev_dy = ctx->ev_io[1], ev_y = ctx->ev_io[2], ev_dx = ctx->ev_io[3];
   uint8_t* b = reinterpret_cast<uint8_t*>(io);
   void *x = b, *y = b + bytes, *gy = b + 2 * bytes, *gx = b + 3 * bytes;
+  const bool bwd = dy_host != nullptr;
   CK(cudaMemcpyAsync(x, x_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
-  if (dy_host) CK(cudaMemcpyAsync(gy, dy_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  if (bwd) {  // queued behind x on the same copy direction
+    CK(cudaEventRecord(ev_x, ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->copy_in, ev_x, 0));
+    CK(cudaMemcpyAsync(gy, dy_host, bytes, cudaMemcpyHostToDevice, ctx->copy_in));
+    CK(cudaEventRecord(ev_dy, ctx->copy_in));
+  }
   forward(x, y);
-  if (dy_host) backward(gy, gx);
-  CK(cudaMemcpyAsync(y_host, y, bytes, cudaMemcpyDeviceToHost, ctx->stream));
-  if (dx_host && dy_host) CK(cudaMemcpyAsync(dx_host, gx, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaEventRecord(ev_y, ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->copy_out, ev_y, 0));
+  CK(cudaMemcpyAsync(y_host, y, bytes, cudaMemcpyDeviceToHost, ctx->copy_out));
+  if (bwd) {
+    CK(cudaStreamWaitEvent(ctx->stream, ev_dy, 0));
+    backward(gy, gx, ev_dx);
+    if (dx_host) {
+      CK(cudaStreamWaitEvent(ctx->copy_out, ev_dx, 0));
+      CK(cudaMemcpyAsync(dx_host, gx, bytes, cudaMemcpyDeviceToHost, ctx->copy_out));
+    }
+  }
+  CK(cudaStreamSynchronize(ctx->copy_out));
   CK(cudaStreamSynchronize(ctx->stream));
 }
 

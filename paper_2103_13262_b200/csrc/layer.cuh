@@ -25,6 +25,8 @@ struct Layer {
   fmoe_plan plan{};
   void *xs = nullptr, *hidden = nullptr, *ys = nullptr;
   bool fwd_done = false;
+  bool routed = false;
+  int prof_slot = -1;   // profiling slot of the current forward (Prof)  // forward_routed: routing injected, no gate on this step
   // backward scratch
   void *d_ys = nullptr, *d_pre = nullptr, *d_xs = nullptr, *d_w = nullptr, *dz = nullptr, *gdx = nullptr;
   __nv_bfloat16* dz_bf16 = nullptr;
@@ -50,7 +52,9 @@ struct Layer {
   fmoe_expert_grads grads() const;
   void init_weights();
   void forward(const void* x, void* y);
-  void backward(const void* dy, void* dx);
+  void forward_routed(const void* x, const int32_t* topk_idx, const void* topk_scores, void* y);
+  void dispatch_and_experts(const void* x, void* y);
+  void backward(const void* dy, void* dx, cudaEvent_t dx_ready = nullptr);
   double train_step(const void* x, const void* target, double lr);
   void sgd(void* param, float* master, const void* grad, int64_t n, double lr, bool weight);
   void step_host(const void* x_host, const void* dy_host, void* y_host, void* dx_host);

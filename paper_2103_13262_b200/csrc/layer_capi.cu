@@ -68,6 +68,20 @@ int fmoe_layer_fwd(fmoe_layer* layer, const void* x, void* y) {
   })
 }
 
+int fmoe_layer_fwd_routed(fmoe_layer* layer, const void* x, const int32_t* topk_idx, const void* topk_scores,
+                          void* y) {
+  FMOE_GUARD({
+    if (!x || !y || !topk_idx || !topk_scores) shape_error("forward_routed: null argument");
+    L(layer)->forward_routed(x, topk_idx, topk_scores, y);
+  })
+}
+
+int fmoe_layer_routing_grad(fmoe_layer* layer, const void** d_topk_scores) {
+  FMOE_GUARD({
+    if (d_topk_scores) *d_topk_scores = L(layer)->d_w;
+  })
+}
+
 int fmoe_layer_bwd(fmoe_layer* layer, const void* dy, void* dx) {
   FMOE_GUARD({
     if (!dy || !dx) shape_error("backward: null dy or dx");

@@ -182,12 +182,22 @@ void gate_bwd(Ctx* ctx, fmoe_dtype t, const void* x, const void* wg, const void*
 }
 
 // ----------------------------------------------------------------- experts
+static void set_route(tc::Params& p, const RowRoute* r) {
+  if (!r) return;
+  p.route_out = r->out;
+  p.route_start = r->start;
+  p.route_rows = r->rows;
+  p.route_dst = r->dst;
+  p.route_world = r->world;
+}
+
 void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
                  const fmoe_expert_params& w, const void* xs, void* hidden, void* ys,
-                 uint32_t* relu_bits, void* preact) {
+                 uint32_t* relu_bits, void* preact, const RowRoute* ys_route) {
   const int64_t E = b.n_experts;
   if (E == 0 || b.capacity == 0) return;
   if (t == FMOE_F64 || t == FMOE_F32) {
+    if (ys_route) shape_error("experts_fwd: routed outputs are bf16-only");
     const auto cnt = host_counts(ctx, b);
     const int64_t max_m = cnt.empty() ? 0 : *std::max_element(cnt.begin(), cnt.end());
     if (max_m == 0) return;
@@ -239,6 +249,7 @@ void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     p.tile_group = b.tile_expert; p.n_mtiles = b.n_tiles; p.b_group_rows = (int)h;
     p.epi = tc::EPI_BF16; p.C = ys; p.ldc = d;
     p.bias = (const float*)w.b2; p.bias_group_stride = d; p.relu = 0;
+    set_route(p, ys_route);
     tc::launch(ctx, 256, false, true, ta, tb, p, max_tiles * ceil_div(d, 256), cg);
     ctx_mark(ctx, MARK_FC2);
   }
@@ -247,10 +258,11 @@ void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
 void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
                  const fmoe_expert_params& w, const void* xs, const void* hidden, const void* d_ys,
                  void* d_xs, const fmoe_expert_grads& g, void* d_pre, float* part_ws,
-                 const uint32_t* relu_bits, const void* mask) {
+                 const uint32_t* relu_bits, const void* mask, int phase, const RowRoute* dxs_route) {
   const int64_t E = b.n_experts;
   if (E == 0) return;
   if (t == FMOE_F64 || t == FMOE_F32) {
+    if (phase != EXPERTS_BWD_ALL || dxs_route) shape_error("experts_bwd: phased / routed backward is bf16-only");
     const auto cnt = host_counts(ctx, b);
     const int64_t max_m = cnt.empty() ? 0 : *std::max_element(cnt.begin(), cnt.end());
     auto run = [&](auto* tag) {
@@ -304,7 +316,8 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
   const int64_t cap = b.capacity;
   const int64_t max_tiles = cap / (128 * cg);  // (pair) row tiles
   const int64_t t128 = cap / 128;              // 128-row tiles (bias partials)
-  {  // dgrad fc2: d_pre = (d_ys W2^T) * (hidden > 0); B(k=c, n=j) = W2[e][j][c] -> K-major [E*h, d]
+  const bool do_dgrad = phase != EXPERTS_BWD_WGRAD, do_wgrad = phase != EXPERTS_BWD_DGRAD;
+  if (do_dgrad) {  // dgrad fc2: d_pre = (d_ys W2^T) * (hidden > 0); B(k=c, n=j) = W2[e][j][c] -> K-major [E*h, d]
     const CUtensorMap ta = tc::make_tmap(d_ys, d, cap, d * 2, 64, 128);
     const CUtensorMap tb = tc::make_tmap(w.w2, d, E * h, d * 2, 64, 256 / cg);
     tc::Params p{};
@@ -316,7 +329,7 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     tc::launch(ctx, 256, false, false, ta, tb, p, max_tiles * ceil_div(h, 256), cg);
     ctx_mark(ctx, MARK_DGRAD2);
   }
-  {  // wgrad fc2: d_w2[e] = hidden_e^T d_ys_e  (M = h, N = d, K = rows of e)
+  if (do_wgrad) {  // wgrad fc2: d_w2[e] = hidden_e^T d_ys_e  (M = h, N = d, K = rows of e)
     const CUtensorMap ta = tc::make_tmap(hidden, h, cap, h * 2, 64, 64);
     const CUtensorMap tb = tc::make_tmap(d_ys, d, cap, d * 2, 64, 64);
     tc::Params p{};
@@ -327,20 +340,23 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
   }
   // d_b2 = colsum(d_ys) per expert (expert.cpp:43-45): tile partials + ordered reduce
   float* part_b2 = part_ws + t128 * h;
-  tile_colsum(ctx, (const __nv_bfloat16*)d_ys, d, b.n_tiles, t128, part_b2);
-  reduce_tile_partials(ctx, part_b2, d, b.offsets, E, (float*)g.d_b2);
-  ctx_mark(ctx, MARK_DB2);
-  {  // dgrad fc1: d_xs = d_pre W1^T; B(k=j, n=c) = W1[e][c][j] -> K-major [E*d, h]
+  if (do_wgrad) {
+    tile_colsum(ctx, (const __nv_bfloat16*)d_ys, d, b.n_tiles, t128, part_b2);
+    reduce_tile_partials(ctx, part_b2, d, b.offsets, E, (float*)g.d_b2);
+    ctx_mark(ctx, MARK_DB2);
+  }
+  if (do_dgrad) {  // dgrad fc1: d_xs = d_pre W1^T; B(k=j, n=c) = W1[e][c][j] -> K-major [E*d, h]
     const CUtensorMap ta = tc::make_tmap(d_pre, h, cap, h * 2, 64, 128);
     const CUtensorMap tb = tc::make_tmap(w.w1, h, E * d, h * 2, 64, 256 / cg);
     tc::Params p{};
     p.mode = tc::RAGGED_M; p.M = (int)cap; p.N = (int)d; p.K = (int)h;
     p.tile_group = b.tile_expert; p.n_mtiles = b.n_tiles; p.b_group_rows = (int)d;
     p.epi = tc::EPI_BF16; p.C = d_xs; p.ldc = d;
+    set_route(p, dxs_route);
     tc::launch(ctx, 256, false, false, ta, tb, p, max_tiles * ceil_div(d, 256), cg);
     ctx_mark(ctx, MARK_DGRAD1);
   }
-  {  // wgrad fc1: d_w1[e] = xs_e^T d_pre_e  (M = d, N = h)
+  if (do_wgrad) {  // wgrad fc1: d_w1[e] = xs_e^T d_pre_e  (M = d, N = h)
     const CUtensorMap ta = tc::make_tmap(xs, d, cap, d * 2, 64, 64);
     const CUtensorMap tb = tc::make_tmap(d_pre, h, cap, h * 2, 64, 64);
     tc::Params p{};
@@ -349,8 +365,10 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     tc::launch(ctx, 256, true, true, ta, tb, p, E * ceil_div(d, 128 * cg) * ceil_div(h, 256), cg);
     ctx_mark(ctx, MARK_WGRAD1);
   }
-  reduce_tile_partials(ctx, part_ws, h, b.offsets, E, (float*)g.d_b1);
-  ctx_mark(ctx, MARK_DB1);
+  if (do_wgrad) {  // d_b1 partials come from the dgrad-fc2 epilogue
+    reduce_tile_partials(ctx, part_ws, h, b.offsets, E, (float*)g.d_b1);
+    ctx_mark(ctx, MARK_DB1);
+  }
 }
 
 int64_t experts_bwd_part_floats(const fmoe_plan& b, int64_t d, int64_t h) {

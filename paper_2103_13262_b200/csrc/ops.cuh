@@ -27,17 +27,38 @@ void gate_dx_bf16(Ctx* ctx, const __nv_bfloat16* dz, const void* wg, int64_t n, 
 
 // relu_bits (optional, bf16): [capacity, h/32] bitmap of hidden > 0 written by
 // fc1 and consumed by experts_bwd instead of re-reading `hidden` for the mask.
+// Fused global_gather target of a bf16 expert GEMM's output rows (see
+// tc::Params::route_out): per (local expert, source rank) chunk of the receive
+// layout, the source rank's buffer and the destination row of the chunk.
+struct RowRoute {
+  void* const* out = nullptr;      // [W] device pointers (peer buffers)
+  const int32_t* start = nullptr;  // [el*W] first receive row of chunk (e, s)
+  const int32_t* rows = nullptr;   // [el*W]
+  const int32_t* dst = nullptr;    // [el*W] first row in source s's send layout
+  int world = 1;
+};
 void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
                  const fmoe_expert_params& w, const void* xs, void* hidden, void* ys,
-                 uint32_t* relu_bits = nullptr, void* preact = nullptr);
+                 uint32_t* relu_bits = nullptr, void* preact = nullptr, const RowRoute* ys_route = nullptr);
 // preact (SIMT dtypes only, optional): also keep x*w1 + b1 before the relu
 // (ForwardCache::preact, expert.hpp:31-35).
 // d_pre_ws: [capacity, h] dtype scratch; mask (SIMT dtypes only, optional): the
 // relu-backward operand, preact (strict > 0, matrix.cpp:147-153), default hidden.
+// Row alignment of bf16 expert blocks for `rows` routed rows over `experts`:
+// 256 (CTA-pair tiles, cta_group::2) once experts average >= 1024 rows, else
+// 128 -- with small experts the 256-row padding would cost more than pairs gain.
+inline int64_t expert_block_align(int64_t rows, int64_t experts) {
+  return rows >= 1024 * experts ? 256 : 128;
+}
+// phase (bf16 only): the data-gradient GEMMs (d_pre, d_xs) and the weight
+// gradients (d_w2, d_b2, d_w1, d_b1) can be issued separately, so d_x is
+// final -- and can leave the GPU -- while the weight gradients still run.
+enum { EXPERTS_BWD_ALL = 0, EXPERTS_BWD_DGRAD = 1, EXPERTS_BWD_WGRAD = 2 };
 void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
                  const fmoe_expert_params& w, const void* xs, const void* hidden, const void* d_ys,
                  void* d_xs, const fmoe_expert_grads& g, void* d_pre_ws, float* part_ws,
-                 const uint32_t* relu_bits = nullptr, const void* mask = nullptr);
+                 const uint32_t* relu_bits = nullptr, const void* mask = nullptr,
+                 int phase = EXPERTS_BWD_ALL, const RowRoute* dxs_route = nullptr);
 // allreduce_sum over ctx's transport (ep.cu): in place, ascending-rank order.
 void allreduce_sum(Ctx* c, fmoe_dtype dt, void* buf, int64_t n, const int* group, int64_t gs);
 

@@ -11,6 +11,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "peer.cuh"
 #include "plan.cuh"
 
 namespace fmoe_b200 {
@@ -57,17 +58,26 @@ __device__ __forceinline__ int64_t pad_row(const fmoe_plan& p, int64_t w) {
 }
 
 // ------------------------------------------------------------------ scatter
-// Pure byte copy: element type only sets the row size.
+// Pure byte copy: element type only sets the row size.  With a route (expert
+// parallelism over peer memory) slot (i, j) is written straight into the
+// receive buffer of its expert's rank: the local scatter and the global
+// scatter (collectives.cpp:146-203) become one pass.
 __global__ void scatter_kernel(const uint8_t* __restrict__ x, int64_t row_bytes, fmoe_plan p,
-                               uint8_t* __restrict__ xs) {
+                               uint8_t* __restrict__ xs, ScatterRoute route) {
   const int64_t w = warp_id_global();
   const int lane = threadIdx.x & 31;
   const int k = (int)p.k;
   if (w < p.n_b) {
     const uint8_t* src = x + w * row_bytes;
-    int64_t dst[8];
+    auto dest = [&](int j) -> uint8_t* {
+      const int64_t pos = __ldg(p.inverse_pos + w * k + j);
+      if (!route.idx) return xs + pos * row_bytes;
+      const int g = __ldg(route.idx + w * k + j);
+      return reinterpret_cast<uint8_t*>(route.dst[__ldg(route.g_rank + g)]) + (pos + __ldg(route.g_delta + g)) * row_bytes;
+    };
+    uint8_t* dst[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) dst[j] = j < k ? (int64_t)__ldg(p.inverse_pos + w * k + j) * row_bytes : 0;
+    for (int j = 0; j < 8; ++j) dst[j] = j < k ? dest(j) : nullptr;
     if ((row_bytes & 15) == 0) {
       const int64_t n16 = row_bytes >> 4;
       const uint4* s4 = reinterpret_cast<const uint4*>(src);
@@ -77,7 +87,7 @@ __global__ void scatter_kernel(const uint8_t* __restrict__ x, int64_t row_bytes,
         for (int u = 0; u < 4; ++u)
           if (c + u * 32 < n16) v[u] = __ldg(s4 + c + u * 32);
         for (int j = 0; j < k; ++j) {
-          uint4* d4 = reinterpret_cast<uint4*>(xs + (j < 8 ? dst[j] : (int64_t)__ldg(p.inverse_pos + w * k + j) * row_bytes));
+          uint4* d4 = reinterpret_cast<uint4*>(j < 8 ? dst[j] : dest(j));
 #pragma unroll
           for (int u = 0; u < 4; ++u)
             if (c + u * 32 < n16) d4[c + u * 32] = v[u];
@@ -86,8 +96,7 @@ __global__ void scatter_kernel(const uint8_t* __restrict__ x, int64_t row_bytes,
     } else {
       for (int64_t c = lane; c < row_bytes; c += 32) {
         const uint8_t v = src[c];
-        for (int j = 0; j < k; ++j)
-          xs[(int64_t)__ldg(p.inverse_pos + w * k + j) * row_bytes + c] = v;
+        for (int j = 0; j < k; ++j) (j < 8 ? dst[j] : dest(j))[c] = v;
       }
     }
     return;
@@ -210,7 +219,7 @@ template <typename T, typename S>
 __global__ void gcb_kernel(const T* __restrict__ dy, const T* __restrict__ ys, int64_t d, fmoe_plan p,
                            const S* __restrict__ w, T* __restrict__ d_ys, S* __restrict__ d_w,
                            const float* __restrict__ scores, const int32_t* __restrict__ topk_idx,
-                           __nv_bfloat16* __restrict__ dz) {
+                           __nv_bfloat16* __restrict__ dz, ScatterRoute route) {
   using A = AccOf<T>;
   constexpr int V = Vec<T>::N;
   const int64_t i = warp_id_global();
@@ -229,6 +238,10 @@ __global__ void gcb_kernel(const T* __restrict__ dy, const T* __restrict__ ys, i
     const int64_t pos = __ldg(p.inverse_pos + i * k + j);
     const A wt = (A)__ldg(w + i * k + j);
     T* dr = d_ys + pos * d;
+    if (route.idx) {  // d_ys rows go straight to the expert ranks (backward global_scatter)
+      const int g = __ldg(route.idx + i * k + j);
+      dr = reinterpret_cast<T*>(route.dst[__ldg(route.g_rank + g)]) + (pos + __ldg(route.g_delta + g)) * d;
+    }
     const T* yr = ys + pos * d;
     A part = A(0);
     if ((d % V) == 0) {
@@ -363,13 +376,15 @@ void reduce_tile_partials(Ctx* ctx, const float* part, int64_t n_cols, const int
   CK_LAUNCH(ctx);
 }
 
-void scatter(Ctx* ctx, fmoe_dtype t, const void* x, int64_t d, const fmoe_plan& p, void* xs) {
+void scatter(Ctx* ctx, fmoe_dtype t, const void* x, int64_t d, const fmoe_plan& p, void* xs,
+             const ScatterRoute* route) {
   const int64_t warps = p.n_b + (p.align > 1 ? p.n_experts * p.align : 0);
   if (warps == 0) return;
   const unsigned grid = (unsigned)ceil_div(warps * 32, 256);
   scatter_kernel<<<grid, 256, 0, ctx->stream>>>(reinterpret_cast<const uint8_t*>(x),
                                                 d * (int64_t)dtype_size(t), p,
-                                                reinterpret_cast<uint8_t*>(xs));
+                                                reinterpret_cast<uint8_t*>(xs),
+                                                route ? *route : ScatterRoute{});
   CK_LAUNCH(ctx);
 }
 
@@ -401,7 +416,8 @@ void scatter_bwd(Ctx* ctx, fmoe_dtype t, const void* d_xs, int64_t d, const fmoe
 
 void gather_combine_bwd(Ctx* ctx, fmoe_dtype t, const void* dy, const void* ys, int64_t d,
                         const fmoe_plan& p, const void* w, void* d_ys, void* d_w,
-                        const void* scores, const int32_t* topk_idx, __nv_bfloat16* dz) {
+                        const void* scores, const int32_t* topk_idx, __nv_bfloat16* dz,
+                        const ScatterRoute* route) {
   const int64_t warps = p.n_b + (p.align > 1 ? p.n_experts * p.align : 0);
   if (warps == 0) return;
   if (dz && p.k > 8) shape_error("fused gate backward supports k <= 8");
@@ -412,7 +428,7 @@ void gather_combine_bwd(Ctx* ctx, fmoe_dtype t, const void* dy, const void* ys, 
     gcb_kernel<T, S><<<grid, 256, 0, ctx->stream>>>(
         reinterpret_cast<const T*>(dy), reinterpret_cast<const T*>(ys), d, p,
         reinterpret_cast<const S*>(w), reinterpret_cast<T*>(d_ys), reinterpret_cast<S*>(d_w),
-        reinterpret_cast<const float*>(scores), topk_idx, dz);
+        reinterpret_cast<const float*>(scores), topk_idx, dz, route ? *route : ScatterRoute{});
   });
   CK_LAUNCH(ctx);
 }

@@ -10,7 +10,11 @@ int64_t plan_scratch_bytes(int64_t n_b, int64_t k, int64_t n_experts);
 void plan_build(Ctx* ctx, const int32_t* topk_idx, const fmoe_plan& p);
 
 // permutes (permute.cu); T = element type, S = score type
-void scatter(Ctx* ctx, fmoe_dtype t, const void* x, int64_t d, const fmoe_plan& p, void* xs);
+struct ScatterRoute;
+// route (optional, expert parallelism over peer memory): write slot rows into
+// the expert ranks' receive buffers instead of xs (see peer.cuh).
+void scatter(Ctx* ctx, fmoe_dtype t, const void* x, int64_t d, const fmoe_plan& p, void* xs,
+             const ScatterRoute* route = nullptr);
 void gather_combine(Ctx* ctx, fmoe_dtype t, const void* ys, int64_t d, const fmoe_plan& p,
                     const void* w, void* y);
 // scatter_backward; d_x[i] = sum_j d_xs[pos(i,j)] (+ addend[i], the gate's d_x).
@@ -20,7 +24,8 @@ void scatter_bwd(Ctx* ctx, fmoe_dtype t, const void* d_xs, int64_t d, const fmoe
 // softmax-Jacobian d_logits row is produced in the same pass (bf16, [n_b, E]).
 void gather_combine_bwd(Ctx* ctx, fmoe_dtype t, const void* dy, const void* ys, int64_t d,
                         const fmoe_plan& p, const void* w, void* d_ys, void* d_w,
-                        const void* scores, const int32_t* topk_idx, __nv_bfloat16* dz);
+                        const void* scores, const int32_t* topk_idx, __nv_bfloat16* dz,
+                        const ScatterRoute* route = nullptr);
 // Bias gradients: out[g][c] = sum over the rows of block g (ascending) of src[row][c].
 void block_colsum(Ctx* ctx, fmoe_dtype t, const void* src, int64_t n_cols, const int32_t* offsets,
                   const int32_t* counts, int64_t n_blocks, void* out);

@@ -239,6 +239,19 @@ __device__ __forceinline__ void epi_store_chunk(const Params& p, const Tile& tl,
     return;
   }
   __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.C) + (int64_t)row * p.ldc + c0;
+  if (p.route_out) {  // fused global_gather: the row goes home over NVLink
+    const int W = p.route_world;
+    out = nullptr;
+    for (int s = 0; s < W; ++s) {
+      const int start = __ldg(p.route_start + tl.g * W + s);
+      if ((unsigned)(row - start) < (unsigned)__ldg(p.route_rows + tl.g * W + s)) {
+        out = reinterpret_cast<__nv_bfloat16*>(p.route_out[s]) +
+              (int64_t)(__ldg(p.route_dst + tl.g * W + s) + row - start) * p.ldc + c0;
+        break;
+      }
+    }
+    if (!out) return;  // pad row
+  }
   uint4* o4 = reinterpret_cast<uint4*>(out);
 #pragma unroll
   for (int q = 0; q < 4; ++q)
@@ -701,7 +714,7 @@ static void launch_t(Ctx* ctx, const CUtensorMap& ta, const CUtensorMap& tb, con
         tc_out = make_tmap(p.C, p.N, rows, p.ldc * 4, 32, 32, 128, true);
         q.tma_out = 1;
       }
-    } else {
+    } else if (!p.route_out) {
       tc_out = make_tmap(p.C, p.N, p.M, p.ldc * 2, 32, 32, 64);
       q.tma_out = 1;
     }

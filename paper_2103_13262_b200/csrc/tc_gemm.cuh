@@ -86,6 +86,17 @@ struct Params {
   uint32_t* relu_bits_out;
   const uint32_t* relu_bits;
   int tma_out;  // set by launch(): outputs leave through TMA stores
+  // Expert parallelism over peer memory (EPI_BF16, RAGGED_M): every output row
+  // is stored straight into the rank that sent it (fused global_gather,
+  // collectives.cpp:205-265).  Row q of expert block g from source s -- rows
+  // [route_start[g*W+s], + route_rows[g*W+s]) -- lands at row
+  // route_dst[g*W+s] + (q - route_start[g*W+s]) of route_out[s]; pad rows are
+  // dropped.
+  void* const* route_out;
+  const int32_t* route_start;
+  const int32_t* route_rows;
+  const int32_t* route_dst;
+  int route_world;
 };
 
 // Host: build a 2-D bf16 tensor map over a row-major [outer, inner] matrix

@@ -90,6 +90,47 @@ def _reverse(rank, world, el, send_counts, recv_counts, recv_buf, so, co, d):
     return out
 
 
+def _fused_push(rank, world, el, align, counts_all, send_buf, d):
+    """The fused global_scatter (peer.cuh) emulated over gloo: every send row
+    goes to rank g_rank[g] at receive row (position + g_delta[g]) as
+    fmoe_ep_routes lays it out."""
+    import paper_2103_13262_b200 as fm
+
+    so, co, bo, rows, gr, gd, rt = fm.ep_routes(world, rank, el, align, counts_all)
+    e = world * el
+    dest_rank = np.repeat(gr, counts_all[rank])
+    dest_row = np.arange(send_buf.shape[0]) + np.repeat(gd, counts_all[rank])
+    out = [torch.from_numpy(np.ascontiguousarray(np.c_[dest_row[dest_rank == p], send_buf[dest_rank == p]]))
+           for p in range(world)]
+    got = [None] * world
+    dist.all_gather_object(got, out)
+    recv = np.zeros((bo[-1], d))
+    for s in range(world):
+        blk = got[s][rank].numpy()
+        recv[blk[:, 0].astype(np.int64)] = blk[:, 1:]
+    return recv, (so, co, bo, rows, gr, gd, rt)
+
+
+def _fused_home(rank, world, el, counts_all, recv_buf, routes, d):
+    """The fused global_gather (the fc2 / dgrad-fc1 epilogue route): receive
+    chunk (e, s) goes back to rank s at route[2][e, s] + offset."""
+    so, co, bo, rows, gr, gd, rt = routes
+    out = [[] for _ in range(world)]
+    for e in range(el):
+        for s in range(world):
+            start, n, dst = int(rt[0, e, s]), int(rt[1, e, s]), int(rt[2, e, s])
+            if n:
+                out[s].append(np.c_[np.arange(dst, dst + n), recv_buf[start:start + n]])
+    out = [torch.from_numpy(np.concatenate(o) if o else np.zeros((0, d + 1))) for o in out]
+    got = [None] * world
+    dist.all_gather_object(got, out)
+    home = np.zeros((int(counts_all[rank].sum()), d))
+    for s in range(world):
+        blk = got[s][rank].numpy()
+        home[blk[:, 0].astype(np.int64)] = blk[:, 1:]
+    return home
+
+
 def _worker(rank, world, port, name, align, q):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -130,6 +171,14 @@ def _worker(rank, world, port, name, align, q):
         dense = np.concatenate([xs_recv[bo[j]:bo[j] + rows[j]] for j in range(el)])
         assert dense.tobytes() == want.tobytes()
         assert all(not xs_recv[bo[j] + rows[j]:bo[j + 1]].any() for j in range(el))  # zero padding
+        # the fused peer-memory routes (fmoe_ep_routes) land every row where the
+        # transport exchange does, from the all-gathered counts alone
+        cl = [torch.zeros(world * el, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(cl, torch.from_numpy(plan["counts"].astype(np.int64)))
+        counts_all = torch.stack(cl).numpy()
+        xs_fused, routes = _fused_push(rank, world, el, align, counts_all, xs_send, d)
+        assert xs_fused.tobytes() == xs_recv.tobytes()
+        assert np.array_equal(routes[0], so) and np.array_equal(routes[1], co) and np.array_equal(routes[2], bo)
         # experts on the received blocks, reverse exchange (C3), combine
         ys_recv = np.zeros_like(xs_recv)
         cache = []
@@ -140,6 +189,7 @@ def _worker(rank, world, port, name, align, q):
             ys_recv[bo[j]:bo[j] + rows[j]] = yj
             cache.append((pre, hid))
         ys_send = _reverse(rank, world, el, send_counts, recv_counts, ys_recv, so, co, d)
+        assert _fused_home(rank, world, el, counts_all, ys_recv, routes, d).tobytes() == ys_send.tobytes()
         y = orc.gather_combine(ys_send, plan, vals)
         assert y.tobytes() == g["y"][rank * n:(rank + 1) * n].tobytes()
         # backward through the same routes

@@ -31,8 +31,8 @@ def fm():
     return m
 
 
-def run_world(fm, world, cfg, dtype, xs, dys):
-    """One thread per rank; returns per-rank dicts of host arrays."""
+def run_world(fm, world, cfg, dtype, xs, dys, exchange="peer", steps=1):
+    """One thread per rank; returns per-rank dicts of host arrays (last step)."""
     w = fm.World(world)
     out = [None] * world
     errs = [None] * world
@@ -44,14 +44,16 @@ def run_world(fm, world, cfg, dtype, xs, dys):
             with torch.cuda.stream(s):
                 layer = fm.MoELayer(cfg, rank=r, dtype=dtype)
                 layer.join(w)
+                layer.set_ep_exchange(exchange)
                 x = xs[r].to(device="cuda", dtype=dtype)
                 dy = dys[r].to(device="cuda", dtype=dtype)
-                y = layer.forward(x)
-                dx = layer.backward(dy)
+                for _ in range(steps):
+                    y = layer.forward(x)
+                    dx = layer.backward(dy)
                 s.synchronize()
                 out[r] = dict(y=y.cpu(), dx=dx.cpu(), dwg=layer.d_wg.cpu(), dw1=layer.grads.d_w1.cpu(),
                               db1=layer.grads.d_b1.cpu(), dw2=layer.grads.d_w2.cpu(), db2=layer.grads.d_b2.cpu(),
-                              idx=layer.routing()[0].cpu())
+                              idx=layer.routing()[0].cpu(), fused=layer.ep_exchange_fused)
                 del layer
         except Exception as e:  # surfaced below
             errs[r] = e
@@ -60,7 +62,7 @@ def run_world(fm, world, cfg, dtype, xs, dys):
     for t in th:
         t.start()
     for t in th:
-        t.join(timeout=300)
+        t.join(timeout=100)
     for e in errs:
         if e is not None:
             raise e
@@ -76,11 +78,13 @@ def single(fm, cfg, dtype, x, dy):
                 dw2=layer.grads.d_w2.cpu(), db2=layer.grads.d_b2.cpu())
 
 
-def check_ep_equals_single(fm, world, n, d, h, el, k, dtype, seed=3):
+def check_ep_equals_single(fm, world, n, d, h, el, k, dtype, seed=3, exchange="peer", steps=1):
     g = torch.Generator().manual_seed(seed)
     xs = [(torch.rand(n, d, generator=g) * 2 - 1).to(dtype) for _ in range(world)]
     dys = [(torch.rand(n, d, generator=g) * 2 - 1).to(dtype) for _ in range(world)]
-    ep = run_world(fm, world, fm.MoEConfig(n, d, h, k, el, world, seed), dtype, xs, dys)
+    ep = run_world(fm, world, fm.MoEConfig(n, d, h, k, el, world, seed), dtype, xs, dys, exchange, steps)
+    # bf16 + peer: the fused exchange (scatter / epilogues over peer memory) ran
+    assert all(o["fused"] == (dtype == torch.bfloat16 and exchange == "peer") for o in ep)
     ref = single(fm, fm.MoEConfig(n * world, d, h, k, el * world, 1, seed), dtype, torch.cat(xs), torch.cat(dys))
     assert torch.equal(torch.cat([o["y"] for o in ep]), ref["y"])
     assert torch.equal(torch.cat([o["dx"] for o in ep]), ref["dx"])
@@ -91,14 +95,22 @@ def check_ep_equals_single(fm, world, n, d, h, el, k, dtype, seed=3):
         assert torch.equal(ep[r]["dwg"], own["dwg"])
 
 
+@pytest.mark.parametrize("exchange", ["peer", "transport"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_ep_bf16_equals_single_worker(fm, world):
-    check_ep_equals_single(fm, world, n=512, d=128, h=256, el=4, k=2, dtype=torch.bfloat16)
+def test_ep_bf16_equals_single_worker(fm, world, exchange):
+    check_ep_equals_single(fm, world, n=512, d=128, h=256, el=4, k=2, dtype=torch.bfloat16, exchange=exchange)
 
 
-def test_ep_bf16_skewed_and_empty_experts(fm):
+@pytest.mark.parametrize("exchange", ["peer", "transport"])
+def test_ep_bf16_skewed_and_empty_experts(fm, exchange):
     """k=1 with few tokens: some experts receive nothing from some (or all) ranks."""
-    check_ep_equals_single(fm, 4, n=40, d=64, h=128, el=2, k=1, dtype=torch.bfloat16, seed=11)
+    check_ep_equals_single(fm, 4, n=40, d=64, h=128, el=2, k=1, dtype=torch.bfloat16, seed=11, exchange=exchange)
+
+
+def test_ep_bf16_pair_tiles_repeated_steps(fm):
+    """>= 1024 rows per local expert: 256-row blocks and CTA-pair GEMMs on the
+    fused path; three steps in a row reuse the peer buffers and epoch flags."""
+    check_ep_equals_single(fm, 2, n=4096, d=128, h=256, el=4, k=2, dtype=torch.bfloat16, seed=5, steps=3)
 
 
 @pytest.mark.parametrize("world", [2, 4])

@@ -324,7 +324,9 @@ def test_layer_f64_vs_golden(fm, orc, name):
         assert err < 1e-13, (key, err)
 
 
-@pytest.mark.parametrize("n,d,h,e,k", [(512, 128, 256, 16, 2), (4096, 256, 512, 32, 2), (1000, 64, 128, 8, 1)])
+# (16384, 128, 256, 8, 2): >= 1024 rows per expert -> 256-row blocks, CTA-pair GEMMs
+@pytest.mark.parametrize("n,d,h,e,k", [(512, 128, 256, 16, 2), (4096, 256, 512, 32, 2), (1000, 64, 128, 8, 1),
+                                       (16384, 128, 256, 8, 2)])
 def test_layer_bf16_vs_oracle(fm, orc, n, d, h, e, k):
     seed = 42
     layer = fm.MoELayer(fm.MoEConfig(n, d, h, k, e, 1, seed), dtype=torch.bfloat16)

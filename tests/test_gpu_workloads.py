@@ -1,0 +1,201 @@
+"""GPU parity of the BASELINE workloads beyond the single gated layer.
+
+* injected (Zipf) routing -- cfg5: FMOE_F64 bit-exact against the oracle's
+  build_plan -> scatter -> expert pool -> gather_combine and its backward
+  (dispatch.cpp:10-126, expert.cpp:24-125); bf16 within the §8c tolerances;
+  at the full cfg5 size (262144 tokens, 256 experts, top-1) the plan is
+  bit-exact against the oracle and outputs / gradients are checked on a token
+  sample and through per-expert sums (size-independent properties);
+* the chained stack -- cfg4: a stack equals its layers applied one by one.
+"""
+import numpy as np
+import pytest
+import torch
+
+from tests.gpu_util import beq, bf16_round, dev, host, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fm():
+    import paper_2103_13262_b200 as m
+
+    return m
+
+
+def oracle_routed(orc, x, dy, idx, vals, w1, b1, w2, b2):
+    """The reference path with the gate replaced by a given IndexMatrix."""
+    e = w1.shape[0]
+    plan = orc.build_plan(idx, e)
+    xs = orc.scatter(x, plan)
+    counts, offs = plan["counts"], plan["offsets"]
+    ys = np.zeros_like(xs)
+    caches = []
+    for g in range(e):
+        a, b = offs[g], offs[g] + counts[g]
+        y_g, pre, hid = orc.expert_forward(xs[a:b], w1[g], b1[g], w2[g], b2[g])
+        ys[a:b] = y_g
+        caches.append((pre, hid))
+    y = orc.gather_combine(ys, plan, vals)
+    d_ys, d_w = orc.gather_combine_backward(dy, ys, plan, vals)
+    d_xs = np.zeros_like(xs)
+    grads = {k: [] for k in ("dw1", "db1", "dw2", "db2")}
+    for g in range(e):
+        a, b = offs[g], offs[g] + counts[g]
+        dx_g, gg = orc.expert_backward(d_ys[a:b], xs[a:b], caches[g][0], caches[g][1], w1[g], w2[g])
+        d_xs[a:b] = dx_g
+        for key in grads:
+            grads[key].append(gg[key])
+    dx = orc.scatter_backward(d_xs, plan)
+    out = dict(y=y, dx=dx, d_w=d_w, plan=plan)
+    out.update({key: np.stack(v) for key, v in grads.items()})
+    return out
+
+
+def _weights(layer):
+    return dict(w1=host(layer.experts.w1), b1=host(layer.experts.b1), w2=host(layer.experts.w2),
+                b2=host(layer.experts.b2))
+
+
+@pytest.mark.parametrize("n,d,h,e,k,s", [(600, 32, 64, 16, 1, 1.0), (777, 64, 96, 8, 2, 1.2), (300, 16, 32, 64, 1, 1.5)])
+def test_routed_f64_bit_exact(fm, orc, n, d, h, e, k, s):
+    from paper_2103_13262_b200.workloads import zipf_routing
+
+    layer = fm.MoELayer(fm.MoEConfig(n, d, h, k, e, 1, 11), dtype=torch.float64)
+    idx, sc = zipf_routing(n, e, k, s, seed=n)
+    x = orc.seeded_matrix(11, 102, n, d)
+    dy = orc.seeded_matrix(11, 103, n, d)
+    y = layer.forward_routed(dev(x), dev(idx, torch.int32), dev(sc.astype(np.float64)))
+    dx = layer.backward(dev(dy))
+    o = oracle_routed(orc, x, dy, idx.astype(np.int64), sc.astype(np.float64), **_weights(layer))
+    assert beq(host(layer.routing()[0]).astype(np.int64), idx.astype(np.int64))
+    assert beq(host(y), o["y"])
+    assert beq(host(dx), o["dx"])
+    assert beq(host(layer.routing_grad()), o["d_w"])
+    for key, got in (("dw1", layer.grads.d_w1), ("db1", layer.grads.d_b1), ("dw2", layer.grads.d_w2),
+                     ("db2", layer.grads.d_b2)):
+        assert beq(host(got), o[key]), key
+    assert not host(layer.d_wg).any()  # no gate on an injected-routing step
+
+
+def test_routed_bf16_zipf(fm, orc):
+    from paper_2103_13262_b200.workloads import zipf_routing
+
+    n, d, h, e, k = 8192, 128, 256, 256, 1
+    layer = fm.MoELayer(fm.MoEConfig(n, d, h, k, e, 1, 3), dtype=torch.bfloat16)
+    idx, sc = zipf_routing(n, e, k, 1.0, seed=5)
+    x = bf16_round(orc.seeded_matrix(3, 102, n, d))
+    dy = bf16_round(orc.seeded_matrix(3, 103, n, d))
+    y = layer.forward_routed(dev(x, torch.bfloat16), dev(idx, torch.int32), dev(sc, torch.float32))
+    dx = layer.backward(dev(dy, torch.bfloat16))
+    torch.cuda.synchronize()
+    o = oracle_routed(orc, x, dy, idx.astype(np.int64), sc.astype(np.float64), **_weights(layer))
+    assert rel_l2(host(y), o["y"]) < 1e-2
+    assert rel_l2(host(dx), o["dx"]) < 2e-2
+    assert rel_l2(host(layer.routing_grad()), o["d_w"]) < 2e-2
+    for key, got in (("dw1", layer.grads.d_w1), ("db1", layer.grads.d_b1), ("dw2", layer.grads.d_w2),
+                     ("db2", layer.grads.d_b2)):
+        assert rel_l2(host(got), o[key]) < 2e-2, key
+
+
+def test_routed_rejects_out_of_range(fm):
+    n, d, h, e, k = 64, 64, 64, 8, 1
+    layer = fm.MoELayer(fm.MoEConfig(n, d, h, k, e, 1, 3), dtype=torch.bfloat16)
+    x = torch.randn(n, d, device="cuda").bfloat16()
+    idx = torch.zeros(n, k, dtype=torch.int32, device="cuda")
+    idx[5, 0] = e
+    sc = torch.ones(n, k, device="cuda")
+    with pytest.raises(fm.ShapeError):  # synchronously, like build_plan (dispatch.cpp:21-23)
+        layer.forward_routed(x, idx, sc)
+    idx[5, 0] = -1
+    with pytest.raises(fm.ShapeError):
+        layer.forward_routed(x, idx, sc)
+    idx[5, 0] = 0
+    y = layer.forward_routed(x, idx, sc)  # the layer is usable after the error
+    layer.backward(torch.ones_like(y))
+    torch.cuda.synchronize()
+    with pytest.raises(fm.ShapeError):
+        layer.forward_routed(x, idx[:, :0], sc)
+
+
+def _expert_ref(x, w1, b1, w2, b2):
+    """One expert in fp32 from bf16 operands, hidden rounded to bf16 as stored."""
+    hid = torch.relu(x.float() @ w1.float() + b1.float()).bfloat16().float()
+    return (hid @ w2.float() + b2.float()).bfloat16().float(), hid
+
+
+def test_cfg5_full_size(fm, orc):
+    """cfg5 at its BASELINE size: 262144 tokens, 256 experts, top-1, d=1024,
+    h=4096, Zipf s=1.  Plan bit-exact; outputs and data gradients on a token
+    sample, bias gradients through per-expert sums."""
+    from paper_2103_13262_b200.workloads import zipf_routing
+
+    n, d, h, e, k = 262144, 1024, 4096, 256, 1
+    torch.cuda.empty_cache()
+    layer = fm.MoELayer(fm.MoEConfig(n, d, h, k, e, 1, 42), dtype=torch.bfloat16)
+    idx, sc = zipf_routing(n, e, k, 1.0, seed=7)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(7)
+    x = (torch.rand(n, d, device="cuda", generator=g) * 2 - 1).bfloat16()
+    dy = (torch.rand(n, d, device="cuda", generator=g) * 2 - 1).bfloat16()
+    it, st = dev(idx, torch.int32), dev(sc, torch.float32)
+    y = layer.forward_routed(x, it, st)
+    dx = layer.backward(dy)
+    torch.cuda.synchronize()
+    # plan: bit-exact against the oracle's build_plan on the same IndexMatrix
+    want = orc.build_plan(idx.astype(np.int64), e)
+    _, _, _, plan = layer.routing()
+    counts = host(fm.api._wrap(plan.counts, (e,), torch.int32, x.device, layer)).astype(np.int64)
+    assert beq(counts, want["counts"])
+    assert counts[0] > 0.15 * n  # the skew is real: ~16% of tokens on expert 0
+    # token sample: y_i = w_i * expert_{e_i}(x_i); dx_i = ((w_i dy_i) W2^T * mask) W1^T
+    rng = np.random.default_rng(0)
+    rows = np.sort(rng.choice(n, 512, replace=False))
+    w1, b1, w2, b2 = layer.experts.w1, layer.experts.b1, layer.experts.w2, layer.experts.b2
+    ys_ref, dx_ref = [], []
+    for r in rows:
+        eid = int(idx[r, 0])
+        yy, hid = _expert_ref(x[r:r + 1], w1[eid], b1[eid], w2[eid], b2[eid])
+        wv = float(sc[r, 0])
+        ys_ref.append(wv * yy)
+        dys = (wv * dy[r:r + 1].float()).bfloat16().float()
+        dpre = ((dys @ w2[eid].float().t()) * (hid > 0)).bfloat16().float()
+        dx_ref.append(dpre @ w1[eid].float().t())
+    ys_ref = torch.cat(ys_ref).cpu().double().numpy()
+    dx_ref = torch.cat(dx_ref).cpu().double().numpy()
+    assert rel_l2(host(y[rows]), ys_ref) < 1e-2
+    assert rel_l2(host(dx[rows]), dx_ref) < 2e-2
+    # d_b2[e] = sum over e's tokens of w_i * dy_i (expert.cpp:43-45)
+    dys_all = (st * dy.float()).bfloat16().float()
+    db2 = torch.zeros(e, d, device="cuda").index_add_(0, it[:, 0].long(), dys_all)
+    assert rel_l2(host(layer.grads.d_b2), host(db2)) < 1e-2
+    # d(topk_scores)_i = <dy_i, ys_i> on the sample
+    dw = host(layer.routing_grad())[rows, 0]
+    dw_ref = (dy[rows].float() * torch.as_tensor(ys_ref / sc[rows], device="cuda").float()).sum(1)
+    assert rel_l2(dw, host(dw_ref)) < 2e-2
+
+
+def test_stack_equals_layers(fm):
+    """cfg4's chained stack (scaled down): forward and backward of the stack
+    equal the layers applied one after another, bit for bit."""
+    from paper_2103_13262_b200.workloads import MoEStack
+
+    n, d, h, el, k, L = 1024, 128, 256, 16, 2, 4
+    cfg = fm.MoEConfig(n, d, h, k, el, 1, 100)
+    stack = MoEStack(cfg, L)
+    x = torch.randn(n, d, device="cuda").bfloat16()
+    dy = torch.randn(n, d, device="cuda").bfloat16()
+    y = stack.forward(x).clone()
+    dx = stack.backward(dy).clone()
+    g_last = stack.layers[-1].grads.d_w1.clone()
+    singles = [fm.MoELayer(fm.MoEConfig(n, d, h, k, el, 1, 100 + i), dtype=torch.bfloat16) for i in range(L)]
+    acts = [x]
+    for s in singles:
+        acts.append(s.forward(acts[-1]).clone())
+    assert torch.equal(acts[-1], y)
+    cur = dy
+    for s in reversed(singles):
+        cur = s.backward(cur).clone()
+    assert torch.equal(cur, dx)
+    assert torch.equal(singles[-1].grads.d_w1, g_last)
