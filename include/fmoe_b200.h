@@ -295,6 +295,14 @@ int fmoe_ep_routes(int world, int rank, int64_t local_experts, int64_t align, co
 #define FMOE_EP_EXCHANGE_PEER 0
 #define FMOE_EP_EXCHANGE_TRANSPORT 1
 int fmoe_layer_set_ep_exchange(fmoe_layer* layer, int mode);
+/* Host-driven peer setup (instead of the automatic one through the
+ * transport): every rank gets its blob (*length bytes; out may be NULL to
+ * query), the host all-gathers them in rank order by any means, and every
+ * rank connects before its first forward.  A connected bf16 layer then runs
+ * expert parallelism with no transport at all.  TransportError if a peer
+ * cannot be mapped. */
+int fmoe_layer_peer_blob(fmoe_layer* layer, void* out, int64_t capacity, int64_t* length);
+int fmoe_layer_peer_connect(fmoe_layer* layer, const void* blobs, int64_t blob_bytes);
 /* *fused = 1 when the last forward ran the fused peer-memory exchange. */
 int fmoe_layer_ep_exchange_fused(fmoe_layer* layer, int* fused);
 

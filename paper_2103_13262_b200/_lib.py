@@ -80,7 +80,7 @@ EXPORTS = [
     "fmoe_a2a_rows_reverse", "fmoe_allreduce_sum", "fmoe_matmul", "fmoe_softmax_rows", "fmoe_topk_rows",
     "fmoe_experts_fwd_cached", "fmoe_experts_bwd_cached", "fmoe_layer_train_step", "fmoe_layer_sync_masters",
     "fmoe_layer_fwd_routed", "fmoe_layer_routing_grad", "fmoe_layer_set_ep_exchange",
-    "fmoe_layer_ep_exchange_fused", "fmoe_ep_routes",
+    "fmoe_layer_ep_exchange_fused", "fmoe_ep_routes", "fmoe_layer_peer_blob", "fmoe_layer_peer_connect",
 ]
 
 
@@ -128,6 +128,8 @@ def _load():
         "fmoe_layer_fwd_routed": [vp, vp, vp, vp, vp],
         "fmoe_layer_routing_grad": [vp, C.POINTER(vp)],
         "fmoe_layer_set_ep_exchange": [vp, C.c_int],
+        "fmoe_layer_peer_blob": [vp, vp, i64, C.POINTER(i64)],
+        "fmoe_layer_peer_connect": [vp, vp, i64],
         "fmoe_ep_routes": [C.c_int, C.c_int, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp],
         "fmoe_layer_ep_exchange_fused": [vp, C.POINTER(C.c_int)],
         "fmoe_world_create": [C.c_int, C.POINTER(vp)],

@@ -538,6 +538,19 @@ class MoELayer:
         """Expert parallelism inside one process (one host thread per rank)."""
         self.ctx.join_world(world, self.rank)
 
+    def connect_peers(self, dist):
+        """bf16 expert parallelism over NVLink peer memory with the peer
+        buffers exchanged through torch.distributed (any backend, gloo
+        included): no device transport is needed afterwards."""
+        n = C.c_int64()
+        check(lib.fmoe_layer_peer_blob(self.h, None, 0, C.byref(n)))
+        buf = (C.c_char * n.value)()
+        check(lib.fmoe_layer_peer_blob(self.h, buf, n.value, C.byref(n)))
+        blobs = [None] * self.config.world_size
+        dist.all_gather_object(blobs, bytes(buf))
+        allb = C.create_string_buffer(b"".join(blobs), n.value * len(blobs))
+        check(lib.fmoe_layer_peer_connect(self.h, allb, n.value))
+
     def set_ep_exchange(self, mode: str):
         """'peer' (default): the expert-parallel row exchanges are fused into
         the scatter / expert-GEMM epilogues over NVLink peer memory;

@@ -294,7 +294,7 @@ static void ep_plan(Layer& L, Transport* tr) {
 static bool ep_use_peer(Layer& L, Transport* tr) {
   Layer::Ep& P = *L.ep;
   if (L.t != FMOE_BF16 || P.exchange != FMOE_EP_EXCHANGE_PEER) return false;
-  if (!P.peer_tried) {
+  if (!P.peer_tried && tr) {
     P.peer_tried = true;
     void* bufs[PB_N] = {P.xs, P.d_ys, L.ys, L.d_xs, P.cnt_mat, P.flags};
     P.peer.connect(L.ctx, tr, bufs, P.peer_scratch, P.peer_table);
@@ -354,10 +354,21 @@ static void ep_plan_peer(Layer& L) {
   P.planned = true;
 }
 
-void Layer::ep_check() const { need_transport(ctx, cfg); }
+// A layer whose peers were connected by the host (fmoe_layer_peer_connect)
+// runs the fused exchange without a transport.
+static bool peer_ready(const Layer& L) {
+  return L.ep && L.ep->peer.ok && L.t == FMOE_BF16 && L.ep->exchange == FMOE_EP_EXCHANGE_PEER;
+}
+
+static Transport* ep_transport(const Layer& L) {
+  if (peer_ready(L) && !L.ctx->transport) return nullptr;
+  return need_transport(L.ctx, L.cfg);
+}
+
+void Layer::ep_check() const { ep_transport(*this); }
 
 void Layer::ep_forward(const void* x, void* y) {
-  Transport* tr = need_transport(ctx, cfg);
+  Transport* tr = ep_transport(*this);
   Ep& P = *ep;
   const int64_t d = cfg.d_m, h = cfg.d_h;
   const size_t rb = (size_t)d * es;
@@ -397,7 +408,7 @@ void Layer::ep_forward(const void* x, void* y) {
 }
 
 void Layer::ep_backward(const void* dy, void* dx) {
-  Transport* tr = need_transport(ctx, cfg);
+  Transport* tr = ep_transport(*this);
   Ep& P = *ep;
   if (!P.planned) protocol_error("backward: no expert-parallel forward cache");
   const int64_t n = cfg.n_b, d = cfg.d_m, h = cfg.d_h, k = cfg.k;
@@ -623,6 +634,35 @@ int fmoe_ep_routes(int world, int rank, int64_t local_experts, int64_t align, co
       shape_error("ep_routes: null buffer");
     ep_routes(world, rank, local_experts, align, counts, send_off, chunk_off, block_off, rows, g_rank, g_delta,
               route);
+  })
+}
+
+int fmoe_layer_peer_blob(fmoe_layer* layer, void* out, int64_t capacity, int64_t* length) {
+  FMOE_GUARD({
+    if (!layer || !length) shape_error("null argument");
+    Layer* l = reinterpret_cast<Layer*>(layer);
+    if (!l->ep || l->t != FMOE_BF16) shape_error("peer_blob: bf16 expert-parallel layers only");
+    *length = (int64_t)PeerSet::blob_bytes();
+    if (out) {
+      if (capacity < *length) shape_error("peer_blob: buffer too small");
+      Layer::Ep& P = *l->ep;
+      void* bufs[PB_N] = {P.xs, P.d_ys, l->ys, l->d_xs, P.cnt_mat, P.flags};
+      PeerSet::make_blob(l->ctx, bufs, out);
+    }
+  })
+}
+
+int fmoe_layer_peer_connect(fmoe_layer* layer, const void* blobs, int64_t blob_bytes) {
+  FMOE_GUARD({
+    if (!layer || !blobs) shape_error("null argument");
+    Layer* l = reinterpret_cast<Layer*>(layer);
+    if (!l->ep || l->t != FMOE_BF16) shape_error("peer_connect: bf16 expert-parallel layers only");
+    if (blob_bytes != (int64_t)PeerSet::blob_bytes()) shape_error("peer_connect: blob size mismatch");
+    Layer::Ep& P = *l->ep;
+    if (P.peer_tried) protocol_error("peer_connect: must be called before the first forward");
+    if (!P.peer.open(l->ctx, P.W, P.r, blobs, P.peer_table))
+      throw Error(FMOE_ERR_TRANSPORT, "peer_connect: a peer's buffers cannot be mapped (no NVLink P2P / other host)");
+    P.peer_tried = true;
   })
 }
 

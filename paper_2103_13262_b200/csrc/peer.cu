@@ -72,50 +72,39 @@ __global__ void put_counts_kernel(const int32_t* __restrict__ counts, int64_t E,
 
 size_t PeerSet::scratch_bytes(int W) { return sizeof(Blob) * (size_t)W + 64 + 4 * (size_t)W; }
 
-void PeerSet::connect(Ctx* ctx, Transport* tr, void* const local[PB_N], void* scratch, void** ptr_table) {
-  close();
-  W = tr->world;
-  r = tr->rank;
+size_t PeerSet::blob_bytes() { return sizeof(Blob); }
+
+void PeerSet::make_blob(Ctx* ctx, void* const local[PB_N], void* out) {
   Blob mine{};
   mine.magic = kMagic;
   mine.host = (int64_t)gethostid();
   mine.pid = (int32_t)getpid();
   mine.device = ctx->device;
-  bool local_ok = true;
   for (int b = 0; b < PB_N; ++b) {
     mine.ptr[b] = reinterpret_cast<uint64_t>(local[b]);
     if (cudaIpcGetMemHandle(&mine.h[b], local[b]) != cudaSuccess) {
       cudaGetLastError();
-      local_ok = false;  // peers of this process can still use the raw pointer
+      std::memset(&mine.h[b], 0, sizeof(mine.h[b]));  // peers of this process can still use the raw pointer
     }
   }
-  // blob exchange over the transport (device buffers: NCCL moves device memory)
-  const size_t B = sizeof(Blob);
-  uint8_t* dev = static_cast<uint8_t*>(scratch);
-  CK(cudaMemcpyAsync(dev + B * r, &mine, B, cudaMemcpyHostToDevice, ctx->stream));
-  std::vector<Xfer> sends, recvs;
-  for (int p = 0; p < W; ++p)
-    if (p != r) {
-      sends.push_back({p, dev + B * r, B});
-      recvs.push_back({p, dev + B * p, B});
-    }
-  tr->group(ctx, sends, recvs);
-  std::vector<Blob> all(W);
-  CK(cudaMemcpyAsync(all.data(), dev, B * W, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  bool good = true;
+  std::memcpy(out, &mine, sizeof(Blob));
+}
+
+bool PeerSet::open(Ctx* ctx, int world, int rank, const void* blobs, void** ptr_table) {
+  close();
+  W = world;
+  r = rank;
+  const Blob* all = static_cast<const Blob*>(blobs);
+  const Blob& mine = all[r];
+  bool good = mine.magic == kMagic;
   for (int b = 0; b < PB_N; ++b) ptr[b].assign(W, nullptr);
   for (int p = 0; p < W && good; ++p) {
     const Blob& o = all[p];
-    if (o.magic != kMagic) {
+    if (o.magic != kMagic || o.host != mine.host) {
       good = false;
       break;
     }
-    const bool same_proc = o.pid == mine.pid && o.host == mine.host;
-    if (!same_proc && (o.host != mine.host || !local_ok)) {
-      good = false;
-      break;
-    }
+    const bool same_proc = o.pid == mine.pid;
     if (o.device != ctx->device) {
       int can = 0;
       cudaDeviceCanAccessPeer(&can, ctx->device, o.device);
@@ -144,38 +133,64 @@ void PeerSet::connect(Ctx* ctx, Transport* tr, void* const local[PB_N], void* sc
       }
     }
   }
-  // pointer tables first (still before the last rendezvous)
-  if (good) {
-    std::vector<void*> flat((size_t)PB_N * W);
-    for (int b = 0; b < PB_N; ++b)
-      for (int p = 0; p < W; ++p) flat[(size_t)b * W + p] = ptr[b][p];
-    CK(cudaMemcpyAsync(ptr_table, flat.data(), flat.size() * sizeof(void*), cudaMemcpyHostToDevice, ctx->stream));
-    for (int b = 0; b < PB_N; ++b) d_ptr[b] = ptr_table + (size_t)b * W;
+  if (!good) {
+    close();
+    return false;
   }
-  // agree: the fused path runs only if every rank mapped every peer
-  int32_t* okv = reinterpret_cast<int32_t*>(dev + B * W + 64);
+  std::vector<void*> flat((size_t)PB_N * W);
+  for (int b = 0; b < PB_N; ++b)
+    for (int p = 0; p < W; ++p) flat[(size_t)b * W + p] = ptr[b][p];
+  CK(cudaMemcpyAsync(ptr_table, flat.data(), flat.size() * sizeof(void*), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int b = 0; b < PB_N; ++b) d_ptr[b] = ptr_table + (size_t)b * W;
+  ok = true;
+  return true;
+}
+
+void PeerSet::connect(Ctx* ctx, Transport* tr, void* const local[PB_N], void* scratch, void** ptr_table) {
+  close();
+  const int world = tr->world, rank = tr->rank;
+  // blob exchange over the transport (device buffers: NCCL moves device memory)
+  const size_t B = sizeof(Blob);
+  std::vector<uint8_t> host(B * world);
+  make_blob(ctx, local, host.data() + B * rank);
+  uint8_t* dev = static_cast<uint8_t*>(scratch);
+  CK(cudaMemcpyAsync(dev + B * rank, host.data() + B * rank, B, cudaMemcpyHostToDevice, ctx->stream));
+  std::vector<Xfer> sends, recvs;
+  for (int p = 0; p < world; ++p)
+    if (p != rank) {
+      sends.push_back({p, dev + B * rank, B});
+      recvs.push_back({p, dev + B * p, B});
+    }
+  tr->group(ctx, sends, recvs);
+  CK(cudaMemcpyAsync(host.data(), dev, B * world, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const bool good = open(ctx, world, rank, host.data(), ptr_table);
+  // agree: the fused path runs only if every rank mapped every peer (nothing
+  // device-synchronising may follow this last rendezvous, see peer.cuh)
+  int32_t* okv = reinterpret_cast<int32_t*>(dev + B * world + 64);
   const int32_t me_ok = good ? 1 : 0;
-  CK(cudaMemcpyAsync(okv + r, &me_ok, 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(okv + rank, &me_ok, 4, cudaMemcpyHostToDevice, ctx->stream));
   sends.clear();
   recvs.clear();
-  for (int p = 0; p < W; ++p)
-    if (p != r) {
-      sends.push_back({p, okv + r, 4});
+  for (int p = 0; p < world; ++p)
+    if (p != rank) {
+      sends.push_back({p, okv + rank, 4});
       recvs.push_back({p, okv + p, 4});
     }
   tr->group(ctx, sends, recvs);
-  std::vector<int32_t> oks(W);
-  CK(cudaMemcpyAsync(oks.data(), okv, 4 * W, cudaMemcpyDeviceToHost, ctx->stream));
+  std::vector<int32_t> oks(world);
+  CK(cudaMemcpyAsync(oks.data(), okv, 4 * world, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  ok = true;
-  for (int p = 0; p < W; ++p) ok = ok && oks[p] == 1;
-  if (!ok) {
+  bool all_ok = true;
+  for (int p = 0; p < world; ++p) all_ok = all_ok && oks[p] == 1;
+  if (!all_ok) {
     close();
     return;
   }
   lw = tr->local_world();
   if (lw) {  // publish this rank's phase events, then rendezvous
-    auto& ev = lw->slots[r].phase;
+    auto& ev = lw->slots[rank].phase;
     if (ev.empty()) {
       ev.resize(PH_N);
       for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

@@ -52,6 +52,13 @@ struct PeerSet {
   // have a stream parked on a flag wait that only this rank can release.
   void connect(Ctx* ctx, Transport* tr, void* const local[PB_N], void* scratch, void** ptr_table);
   static size_t scratch_bytes(int W);
+  // The same in two halves for hosts that exchange the blobs themselves
+  // (fmoe_layer_peer_blob / fmoe_layer_peer_connect): this rank's blob, and
+  // opening every rank's blob (rank order).  open() returns false (and leaves
+  // ok = false) if any peer cannot be mapped.
+  static size_t blob_bytes();
+  static void make_blob(Ctx* ctx, void* const local[PB_N], void* out);
+  bool open(Ctx* ctx, int world, int rank, const void* blobs, void** ptr_table);
   void close();
   // Kernel-side flag write: epoch into slot (phase, r) of every peer's flags.
   void signal(Ctx* ctx, int phase);

@@ -26,9 +26,12 @@ struct Cfg {
   static constexpr int NBUF = EPI == EPI_F32 ? 1 : 2;
   static constexpr int TILE_BYTES = 32 * OUT_ROW_BYTES;
   static constexpr int STORE_BYTES = TMA_STORE ? 8 * NBUF * TILE_BYTES : 0;
-  static constexpr int BUDGET = 200 * 1024 - STORE_BYTES - COLSUM_BYTES;
+  // bf16 epilogues stage the bias of each warp's 128-column slice of the tile
+  static constexpr int BIAS_BYTES = EPI == EPI_BF16 ? 8 * (BN / 2) * 4 : 0;
+  static constexpr int BUDGET = 200 * 1024 - STORE_BYTES - COLSUM_BYTES - BIAS_BYTES;
   static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + STORE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + COLSUM_BYTES;
+  static constexpr int SMEM =
+      STAGES * STAGE_BYTES + STORE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + COLSUM_BYTES + BIAS_BYTES;
 };
 
 // Named barrier among the 4 epilogue warps (ids 1.. are free; 0 = __syncthreads).
@@ -342,6 +345,81 @@ __device__ __forceinline__ void epi_gate(const Params& p, uint32_t tbase, int ro
   }
 }
 
+// Lean drain of one tile for the bf16 expert GEMMs (every row valid, N a
+// multiple of BN, TMA-store output): the transforms are selected at compile
+// time so a 32-column chunk costs ~one instruction per value per transform.
+//   BIAS  += bias (staged in shared memory once per tile)
+//   RELU  max(v, 0) and, when p.relu_bits_out, its bitmap (bit = v > 0)
+//   MASK  v * bit of p.relu_bits (relu_backward, strict >)
+//   COLSUM per-column sums of the final values into colsum_smem
+template <int BN, int NBUF, bool BIAS, bool RELU, bool MASK, bool COLSUM>
+__device__ __forceinline__ void drain_bf16(const Params& p, const Tile& tl, const CUtensorMap* tmC, uint32_t tbase,
+                                           int c_lo, int row, int out_row, uint32_t stage_base, uint32_t& sbuf,
+                                           const float* bias_s, float* colsum_smem, int q, int lane) {
+  constexpr int CPW = BN / 64;
+  constexpr uint32_t TILE_BYTES = 32 * 64;
+  uint32_t mbits[CPW];
+  if constexpr (MASK) {
+#pragma unroll
+    for (int i = 0; i < CPW; ++i) mbits[i] = __ldg(p.relu_bits + relu_bits_index(row, tl.n0 + (c_lo + i) * 32, p.N));
+  }
+  uint32_t buf[2][32];
+  tmem_ld_issue(tbase + c_lo * 32, buf[0]);
+#pragma unroll
+  for (int i = 0; i < CPW; ++i) {
+    const int c = c_lo + i;
+    tmem_ld_wait(buf[i & 1]);
+    if (i + 1 < CPW) tmem_ld_issue(tbase + (c + 1) * 32, buf[(i + 1) & 1]);
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(buf[i & 1][j]);
+    if constexpr (BIAS) {
+      const float4* b4 = reinterpret_cast<const float4*>(bias_s + i * 32);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 bb = b4[j];
+        v[4 * j] += bb.x; v[4 * j + 1] += bb.y; v[4 * j + 2] += bb.z; v[4 * j + 3] += bb.w;
+      }
+    }
+    if constexpr (RELU) {
+      uint32_t bits = 0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        v[j] = fmaxf(v[j], 0.f);  // v >= +0 afterwards: v > 0 <=> its bits are nonzero
+        bits |= ((__float_as_uint(v[j]) + 0x7FFFFFFFu) >> 31) << j;
+      }
+      if (p.relu_bits_out) p.relu_bits_out[relu_bits_index(row, tl.n0 + c * 32, p.N)] = bits;
+    }
+    if constexpr (MASK) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = ((mbits[i] >> j) & 1u) ? v[j] : 0.f;
+    }
+    const uint32_t stage = stage_base + sbuf * TILE_BYTES;
+    if (lane == 0) bulk_wait_read<NBUF - 1>();
+    __syncwarp();
+    {
+      const uint32_t r = (uint32_t)lane;
+      const uint32_t base = stage + r * 64;
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) {
+        const uint32_t a = base + (((uint32_t)qq ^ ((r >> 1) & 3u)) << 4);
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+                     "r"(pack_bf16(v[qq * 8 + 0], v[qq * 8 + 1])), "r"(pack_bf16(v[qq * 8 + 2], v[qq * 8 + 3])),
+                     "r"(pack_bf16(v[qq * 8 + 4], v[qq * 8 + 5])), "r"(pack_bf16(v[qq * 8 + 6], v[qq * 8 + 7]))
+                     : "memory");
+      }
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(tmC, stage, tl.n0 + c * 32, out_row);
+      bulk_commit();
+    }
+    sbuf = (sbuf + 1) % NBUF;
+    if constexpr (COLSUM) colsum_smem[q * BN + c * 32 + lane] = warp_transpose_sum(v, lane);
+  }
+}
+
 // ------------------------------------------------------------------ kernel
 template <int BN, bool A_MN, bool B_MN, int CG, int EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
@@ -366,6 +444,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* colsum_smem = reinterpret_cast<float*>(sOut + C::STORE_BYTES + 256);
+  float* bias_smem = reinterpret_cast<float*>(sOut + C::STORE_BYTES + 256 + C::COLSUM_BYTES);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -561,6 +640,47 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4) out[q4] = o[q4];
           }
+        }
+      } else if ((EPI == EPI_BF16 || EPI == EPI_MASK_BF16) && C::TMA_STORE && p.tma_out && (p.N % BN) == 0 &&
+                 tl.m0 + BM * CG <= p.M && (EPI != EPI_MASK_BF16 || p.relu_bits) &&
+                 (EPI != EPI_BF16 || p.relu || !p.relu_bits_out)) {
+        // fast path (the expert GEMMs): compile-time transforms, see drain_bf16
+        const uint32_t stage_base = smem_u32(sOut) + (uint32_t)(ew * C::NBUF * C::TILE_BYTES);
+        const int out_row = tl.m0 + row_off + q * 32;
+        float* bias_s = bias_smem + ew * (BN / 2);
+        if constexpr (EPI == EPI_BF16) {
+          if (p.bias) {  // this warp's 128 bias columns -> shared memory, once per tile
+            const float4 bb = __ldg(reinterpret_cast<const float4*>(p.bias + (int64_t)tl.g * p.bias_group_stride +
+                                                                   tl.n0 + c_lo * 32) + lane);
+            reinterpret_cast<float4*>(bias_s)[lane] = bb;
+            __syncwarp();
+            if (p.relu)
+              drain_bf16<BN, C::NBUF, true, true, false, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
+                                                                sbuf, bias_s, colsum_smem, q, lane);
+            else
+              drain_bf16<BN, C::NBUF, true, false, false, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
+                                                                 sbuf, bias_s, colsum_smem, q, lane);
+          } else if (p.relu) {
+            drain_bf16<BN, C::NBUF, false, true, false, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
+                                                               sbuf, bias_s, colsum_smem, q, lane);
+          } else {
+            drain_bf16<BN, C::NBUF, false, false, false, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
+                                                                sbuf, bias_s, colsum_smem, q, lane);
+          }
+        } else {
+          if (p.colsum_part)
+            drain_bf16<BN, C::NBUF, false, false, true, true>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
+                                                              sbuf, bias_s, colsum_smem, q, lane);
+          else
+            drain_bf16<BN, C::NBUF, false, false, true, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
+                                                               sbuf, bias_s, colsum_smem, q, lane);
+        }
+        if (p.colsum_part) {
+          epi_bar();
+          for (int col = ew * 32 + lane; col < BN; col += 256)
+            p.colsum_part[(int64_t)((tl.m0 + row_off) / BM) * p.N + tl.n0 + col] =
+                colsum_smem[col] + colsum_smem[BN + col] + colsum_smem[2 * BN + col] + colsum_smem[3 * BN + col];
+          epi_bar();
         }
       } else {
         // Software-pipelined drain: the TMEM load of chunk i+1 is in flight
