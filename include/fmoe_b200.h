@@ -252,6 +252,21 @@ int fmoe_layer_step_host(fmoe_layer* layer, const void* x_host, const void* dy_h
 int fmoe_layer_train_step(fmoe_layer* layer, const void* x, const void* target, double lr, double* loss);
 int fmoe_layer_sync_masters(fmoe_layer* layer);
 
+/* Weight checkpoints in the reference's file format ("FMOE-CKPT" v1, f64,
+ * checkpoint.hpp:10-16, checkpoint.cpp:63-122).  info reads the header;
+ * load_checkpoint reads the gate and this rank's experts straight into the
+ * layer (ShapeError unless d_m, d_h and the total expert count match; values
+ * rounded once to the layer dtype); save_checkpoint writes every expert and
+ * so needs a world_size 1 layer (ShapeError otherwise, as save_checkpoint's
+ * expert-list check).  ProtocolError for unreadable / malformed files. */
+typedef struct {
+  int64_t n_b, d_m, d_h, k, n_e_local, world_size, experts_total;
+  uint64_t seed;
+} fmoe_ckpt_info;
+int fmoe_checkpoint_info(const char* path, fmoe_ckpt_info* out);
+int fmoe_layer_load_checkpoint(fmoe_layer* layer, const char* path);
+int fmoe_layer_save_checkpoint(fmoe_layer* layer, const char* path);
+
 /* --------------------------------------------- expert parallelism (L2, EP) */
 /* A context's transport replaces the reference's Transport (transport.hpp:18-38).
  * Communicator over NCCL (NVLink/NVSwitch), one process per GPU: rank 0

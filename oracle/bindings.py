@@ -320,6 +320,30 @@ class Ref(_Lib):
         f(seed, _ptr(out), n, lo, hi)
         return out
 
+    def save_checkpoint(self, path, w, n_b=0, k=1, n_e_local=None, world=1, seed=0):
+        """save_checkpoint (checkpoint.cpp:63-92) of the weight dict w."""
+        e, d, h = w["w1"].shape
+        meta = np.array([n_b, k, e if n_e_local is None else n_e_local, world, seed], np.int64)
+        f = self.lib.ref_save_checkpoint
+        f.restype = C.c_int
+        f.argtypes = [C.c_char_p, _i64, _i64, _i64] + [_vp] * 6
+        self.check(f(path.encode(), d, h, e, _ptr(meta),
+                     *[_ptr(_arr(w[key], np.float64)) for key in ("wg", "w1", "b1", "w2", "b2")]))
+
+    def load_checkpoint(self, path):
+        """load_checkpoint (checkpoint.cpp:94-122) -> (header dict, weight dict)."""
+        f = self.lib.ref_load_checkpoint
+        f.restype = C.c_int
+        f.argtypes = [C.c_char_p] + [_vp] * 6
+        hd = np.zeros(7, np.int64)
+        self.check(f(path.encode(), _ptr(hd), None, None, None, None, None))
+        n_b, d, h, k, el, world, seed = (int(v) for v in hd)
+        e = el * world
+        w = dict(wg=np.empty((d, e)), w1=np.empty((e, d, h)), b1=np.empty((e, h)), w2=np.empty((e, h, d)),
+                 b2=np.empty((e, d)))
+        self.check(f(path.encode(), _ptr(hd), *[_ptr(w[key]) for key in ("wg", "w1", "b1", "w2", "b2")]))
+        return dict(n_b=n_b, d_m=d, d_h=h, k=k, n_e_local=el, world_size=world, seed=seed), w
+
     def init_state(self, seed, d, h, e, k=1):
         wg = np.empty((d, e)); w1 = np.empty((e, d, h)); b1 = np.empty((e, h))
         w2 = np.empty((e, h, d)); b2 = np.empty((e, d))
@@ -466,6 +490,16 @@ class Ref(_Lib):
                   _arr(b2, np.float64), out["y"], g("dx"), g("dwg"), g("dw1"), g("db1"), g("dw2"),
                   g("db2"), out["send_counts"], out["recv_counts"])
         return out
+
+    def toy_task(self, n, d, h, k, e_local, world, seed):
+        """make_toy_task -> (inputs, targets), [n*world, d] each."""
+        x = np.empty((n * world, d))
+        t = np.empty((n * world, d))
+        f = self.lib.ref_toy_task
+        f.restype = C.c_int
+        f.argtypes = [_i64] * 6 + [_u64, _vp, _vp]
+        self.check(f(n, d, h, k, e_local, world, seed, _ptr(x), _ptr(t)))
+        return x, t
 
     def train_steps(self, x, target, world, n, h, e_local, k, seed, steps, lr):
         """ref_train_steps: the reference's train_step trajectory (x/target are

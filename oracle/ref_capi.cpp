@@ -17,6 +17,7 @@
 #include <thread>
 #include <vector>
 
+#include "fmoe/checkpoint.hpp"
 #include "fmoe/collectives.hpp"
 #include "fmoe/dispatch.hpp"
 #include "fmoe/errors.hpp"
@@ -433,6 +434,69 @@ int ref_bench_step(void* handle) {
 }
 
 void ref_bench_destroy(void* handle) { delete static_cast<RefBench*>(handle); }
+
+// make_toy_task (moe_layer.cpp): inputs / targets [n_b * world, d_m].
+int ref_toy_task(int64_t n, int64_t d, int64_t h, int64_t k, int64_t el, int64_t world, uint64_t seed, double* x,
+                 double* t) {
+  return guarded([&] {
+    MoEConfig cfg;
+    cfg.n_b = static_cast<std::size_t>(n);
+    cfg.d_m = static_cast<std::size_t>(d);
+    cfg.d_h = static_cast<std::size_t>(h);
+    cfg.k = static_cast<std::size_t>(k);
+    cfg.n_e_local = static_cast<std::size_t>(el);
+    cfg.world_size = static_cast<std::size_t>(world);
+    cfg.seed = seed;
+    const ToyTask task = make_toy_task(cfg);
+    out_matrix(task.inputs, x);
+    out_matrix(task.targets, t);
+  });
+}
+
+// save_checkpoint (checkpoint.cpp:63-92) of the given weights: wg [d, e],
+// w1 [e, d, h], b1 [e, h], w2 [e, h, d], b2 [e, d]; meta = n_b, k,
+// n_e_local, world_size, seed.
+int ref_save_checkpoint(const char* path, int64_t d, int64_t h, int64_t e, const int64_t* meta,
+                        const double* wg, const double* w1, const double* b1, const double* w2,
+                        const double* b2) {
+  return guarded([&] {
+    MoEConfig cfg;
+    cfg.n_b = static_cast<std::size_t>(meta[0]);
+    cfg.d_m = static_cast<std::size_t>(d);
+    cfg.d_h = static_cast<std::size_t>(h);
+    cfg.k = static_cast<std::size_t>(meta[1]);
+    cfg.n_e_local = static_cast<std::size_t>(meta[2]);
+    cfg.world_size = static_cast<std::size_t>(meta[3]);
+    cfg.seed = static_cast<uint64_t>(meta[4]);
+    std::vector<ExpertParams> ex;
+    for (int64_t g = 0; g < e; ++g)
+      ex.push_back(ExpertParams{to_matrix(w1 + g * d * h, d, h), to_matrix(b1 + g * h, 1, h),
+                                to_matrix(w2 + g * h * d, h, d), to_matrix(b2 + g * d, 1, d), ParamTag::NoSync});
+    save_checkpoint(path, cfg, GateParams{to_matrix(wg, d, e), ParamTag::World}, ex);
+  });
+}
+
+// load_checkpoint (checkpoint.cpp:94-122): header (n_b, d_m, d_h, k,
+// n_e_local, world_size, seed) and the weights (shapes as above).
+int ref_load_checkpoint(const char* path, int64_t* header, double* wg, double* w1, double* b1, double* w2,
+                        double* b2) {
+  return guarded([&] {
+    const Checkpoint c = load_checkpoint(path);
+    const MoEConfig& k = c.config;
+    const int64_t hv[7] = {(int64_t)k.n_b, (int64_t)k.d_m, (int64_t)k.d_h, (int64_t)k.k,
+                           (int64_t)k.n_e_local, (int64_t)k.world_size, (int64_t)k.seed};
+    std::memcpy(header, hv, sizeof(hv));
+    if (!wg) return;
+    const std::size_t d = k.d_m, h = k.d_h;
+    out_matrix(c.gate.w_g, wg);
+    for (std::size_t g = 0; g < c.experts.size(); ++g) {
+      out_matrix(c.experts[g].w1, w1 + g * d * h);
+      out_matrix(c.experts[g].b1, b1 + g * h);
+      out_matrix(c.experts[g].w2, w2 + g * h * d);
+      out_matrix(c.experts[g].b2, b2 + g * d);
+    }
+  });
+}
 
 // Injected-routing CPU baseline: the reference's dispatch +
 // expert pool with a given IndexMatrix and scores instead of its gate --

@@ -19,6 +19,7 @@ from .api import (  # noqa: F401
     TransportError,
     alloc_plan,
     build_plan,
+    checkpoint_info,
     gate_backward,
     gate_forward,
     gather_combine,

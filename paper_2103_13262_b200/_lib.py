@@ -81,7 +81,13 @@ EXPORTS = [
     "fmoe_experts_fwd_cached", "fmoe_experts_bwd_cached", "fmoe_layer_train_step", "fmoe_layer_sync_masters",
     "fmoe_layer_fwd_routed", "fmoe_layer_routing_grad", "fmoe_layer_set_ep_exchange",
     "fmoe_layer_ep_exchange_fused", "fmoe_ep_routes", "fmoe_layer_peer_blob", "fmoe_layer_peer_connect",
+    "fmoe_checkpoint_info", "fmoe_layer_load_checkpoint", "fmoe_layer_save_checkpoint",
 ]
+
+
+class CkptInfo(C.Structure):
+    _fields_ = [("n_b", i64), ("d_m", i64), ("d_h", i64), ("k", i64), ("n_e_local", i64), ("world_size", i64),
+                ("experts_total", i64), ("seed", C.c_uint64)]
 
 
 class ExchangePlanC(C.Structure):
@@ -130,6 +136,9 @@ def _load():
         "fmoe_layer_set_ep_exchange": [vp, C.c_int],
         "fmoe_layer_peer_blob": [vp, vp, i64, C.POINTER(i64)],
         "fmoe_layer_peer_connect": [vp, vp, i64],
+        "fmoe_checkpoint_info": [C.c_char_p, C.POINTER(CkptInfo)],
+        "fmoe_layer_load_checkpoint": [vp, C.c_char_p],
+        "fmoe_layer_save_checkpoint": [vp, C.c_char_p],
         "fmoe_ep_routes": [C.c_int, C.c_int, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp],
         "fmoe_layer_ep_exchange_fused": [vp, C.POINTER(C.c_int)],
         "fmoe_world_create": [C.c_int, C.POINTER(vp)],

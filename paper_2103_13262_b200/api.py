@@ -221,6 +221,13 @@ def ep_routes(world: int, rank: int, local_experts: int, align: int, counts):
     return so, co.reshape(local_experts, world), bo, rows, gr, gd, rt.reshape(3, local_experts, world)
 
 
+def checkpoint_info(path: str) -> dict:
+    """Header of a reference checkpoint file (fmoe_checkpoint_info)."""
+    info = _lib.CkptInfo()
+    check(lib.fmoe_checkpoint_info(str(path).encode(), C.byref(info)))
+    return {k: int(getattr(info, k)) for k, _ in info._fields_}
+
+
 def _ctx(t: torch.Tensor) -> Context:
     return Context.get(t.device)
 
@@ -528,6 +535,15 @@ class MoELayer:
     def init_weights(self):
         """init_state (moe_layer.cpp:28-45): the reference's generators."""
         check(lib.fmoe_layer_init_weights(self.h))
+
+    def load_checkpoint(self, path: str):
+        """Gate + this rank's experts from a reference checkpoint file
+        (FMOE-CKPT v1, checkpoint.cpp:94-122), rounded once to the layer dtype."""
+        check(lib.fmoe_layer_load_checkpoint(self.h, str(path).encode()))
+
+    def save_checkpoint(self, path: str):
+        """All weights in the reference's checkpoint format (world_size 1)."""
+        check(lib.fmoe_layer_save_checkpoint(self.h, str(path).encode()))
 
     def connect(self, dist):
         """Expert parallelism over NCCL: one process per GPU, torch.distributed

@@ -58,6 +58,8 @@ struct Layer {
   double train_step(const void* x, const void* target, double lr);
   void sgd(void* param, float* master, const void* grad, int64_t n, double lr, bool weight);
   void step_host(const void* x_host, const void* dy_host, void* y_host, void* dx_host);
+  void load_checkpoint(const char* path);  // checkpoint.cu
+  void save_checkpoint(const char* path);
   void ep_alloc();
   void ep_check() const;  // ProtocolError unless a matching transport is attached
   void ep_forward(const void* x, void* y);

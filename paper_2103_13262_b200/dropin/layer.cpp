@@ -11,6 +11,7 @@
 
 #include "dropin.hpp"
 #include "fmoe/checkpoint.hpp"
+#include "ckpt.h"
 #include "fmoe/collectives.hpp"
 #include "fmoe/errors.hpp"
 #include "fmoe/moe_layer.hpp"
@@ -403,11 +404,78 @@ ToyTask make_toy_task(const MoEConfig& config) {
 }
 
 // ------------------------------------------------------------ checkpoint
-void save_checkpoint(const std::string& path, const MoEConfig&, const GateParams&, std::span<const ExpertParams>) {
-  throw ProtocolError("save_checkpoint(" + path + "): checkpoint files are not part of the B200 drop-in");
+// The reference's file format through the shared codec (csrc/ckpt.h); the
+// Matrix values are written / read bit for bit (f64).
+namespace {
+[[noreturn]] void ckpt_rethrow(const fmoe_b200::ckpt::CkptError& e) {
+  if (e.code == fmoe_b200::ckpt::SHAPE) throw ShapeError(e.msg);
+  throw ProtocolError(e.msg);
 }
+void ckpt_write(fmoe_b200::ckpt::Writer& out, const Matrix& m) { out.matrix(m.rows(), m.cols(), m.data()); }
+Matrix ckpt_read(fmoe_b200::ckpt::Reader& in, const char* what) {
+  uint64_t r = 0, c = 0;
+  std::vector<double> v = in.matrix_any(&r, &c, what);
+  Matrix m(r, c);
+  std::copy(v.begin(), v.end(), m.data());
+  return m;
+}
+}  // namespace
+
+void save_checkpoint(const std::string& path, const MoEConfig& config, const GateParams& gate,
+                     std::span<const ExpertParams> experts) {
+  if (experts.size() != config.total_experts())
+    throw ShapeError("save_checkpoint: expert list must cover every global index");
+  try {
+    fmoe_b200::ckpt::Writer out(path);
+    fmoe_b200::ckpt::Header h;
+    h.n_b = config.n_b;
+    h.d_m = config.d_m;
+    h.d_h = config.d_h;
+    h.k = config.k;
+    h.n_e_local = config.n_e_local;
+    h.world_size = config.world_size;
+    h.experts = config.total_experts();
+    h.seed = config.seed;
+    out.header(h);
+    ckpt_write(out, gate.w_g);
+    for (const ExpertParams& e : experts) {
+      ckpt_write(out, e.w1);
+      ckpt_write(out, e.b1);
+      ckpt_write(out, e.w2);
+      ckpt_write(out, e.b2);
+    }
+    out.close();
+  } catch (const fmoe_b200::ckpt::CkptError& e) {
+    ckpt_rethrow(e);
+  }
+}
+
 Checkpoint load_checkpoint(const std::string& path) {
-  throw ProtocolError("load_checkpoint(" + path + "): checkpoint files are not part of the B200 drop-in");
+  Checkpoint c;
+  try {
+    fmoe_b200::ckpt::Reader in(path);
+    const fmoe_b200::ckpt::Header h = in.header();
+    c.config.n_b = h.n_b;
+    c.config.d_m = h.d_m;
+    c.config.d_h = h.d_h;
+    c.config.k = h.k;
+    c.config.n_e_local = h.n_e_local;
+    c.config.world_size = h.world_size;
+    c.config.seed = h.seed;
+    c.gate.w_g = ckpt_read(in, "gate w_g");
+    c.gate.tag = ParamTag::World;
+    c.experts.resize(h.experts);
+    for (auto& e : c.experts) {
+      e.w1 = ckpt_read(in, "expert w1");
+      e.b1 = ckpt_read(in, "expert b1");
+      e.w2 = ckpt_read(in, "expert w2");
+      e.b2 = ckpt_read(in, "expert b2");
+      e.tag = ParamTag::NoSync;
+    }
+  } catch (const fmoe_b200::ckpt::CkptError& e) {
+    ckpt_rethrow(e);
+  }
+  return c;
 }
 
 }  // namespace fmoe

@@ -6,8 +6,8 @@ moe_layer}.cpp from the reference checkout with a minimal doctest stand-in
 (tests/dropin/doctest.h); the binaries travel to the GPU box with the
 snapshot.  Every operator they call runs on the GPU in the FMOE_F64 parity mode.
 
-Excluded test cases (out of the accelerated path):
-  * "checkpoint round trip" -- checkpoint files are not part of the drop-in.
+Every test case runs (the checkpoint round trip included: the drop-in reads
+and writes the reference's file format).
 """
 import os
 import subprocess
@@ -18,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "tests", "dropin", "_bin")
 LIB = os.path.join(ROOT, "paper_2103_13262_b200", "libfmoe_dropin.so")
 SUITES = ["test_tensor", "test_gate", "test_dispatch", "test_expert", "test_moe_layer"]
-EXCLUDE = {"test_moe_layer": ["checkpoint round trip"]}
+EXCLUDE = {}
 
 
 def test_dropin_library_exports_reference_api():

@@ -20,9 +20,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 
+# issue order of one bf16 single-GPU step (layer.cu): data gradients first
 STEP_ORDER = ["gate", "plan_hist", "plan_scan", "plan_rank", "scatter", "fc1", "fc2", "gather_combine",
-              "gcb", "dgrad_fc2", "wgrad_fc2", "db2_colsum", "db2_reduce", "dgrad_fc1", "wgrad_fc1", "db1_reduce",
-              "gate_dwg_offsets", "gate_dwg", "gate_dwg_reduce", "gate_dx"]
+              "gcb", "dgrad_fc2", "dgrad_fc1", "gate_dx", "scatter_bwd", "wgrad_fc2", "db2_colsum", "db2_reduce",
+              "wgrad_fc1", "db1_reduce", "gate_dwg_offsets", "gate_dwg", "gate_dwg_reduce"]
 
 
 def short(name):
@@ -43,13 +44,13 @@ def launches(tag):
         d = per.setdefault(key, {"name": short(r[h["Kernel Name"]]), "grid": r[h["Grid Size"]]})
         d[r[h["Metric Name"]]] = float(r[h["Metric Value"]].replace(",", ""))
     ids = sorted(per)
-    # one step = the 20 launches starting at the first gate GEMM (tc_gemm_kernel<64|128|256, 0, 1, 1, 3>)
+    # one step = the launches starting at the first gate GEMM (tc_gemm_kernel<64|128|256, 0, 1, 1, 3>)
     first = next(i for i in ids if "tc_gemm_kernel<" in per[i]["name"] and per[i]["name"].endswith(", 3>"))
     step = [per[i] for i in ids if i >= first][:len(STEP_ORDER)]
     total = sum(s["gpu__time_duration.sum"] for s in step)
     lines = [f"# {tag}: kernel launches of one bench step (cfg2, ncu --clock-control none, serialized)", "",
              "Command: `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
-             "--clock-control none python bench.py --steps 2 --warmup 3` (tools/gpu_profile.sh).  "
+             "--clock-control none python bench.py --steps 2 --warmup 3 --e2e-steps 1` (tools/gpu_profile.sh).  "
              "Per-launch times are cold-cache and serialized; compare shares, not absolutes.", "",
              "| # | stage | kernel | grid | time (us) | share | DRAM read (MB) | DRAM write (MB) |",
              "|---|---|---|---|---|---|---|---|"]
