@@ -50,6 +50,7 @@ struct Layer::Ep {
   void* peer_scratch = nullptr; // connect's blob exchange
   void** peer_table = nullptr;  // [PB_N][W] device pointer tables
   bool fused = false;           // the current step runs the fused path
+  bool device_plan = false;     // its layouts were computed on the device
 };
 
 namespace {
@@ -302,6 +303,105 @@ static bool ep_use_peer(Layer& L, Transport* tr) {
   return P.peer.ok;
 }
 
+// Device-side layouts for the fused path (the host arithmetic of
+// ep_routes + the receive block plan of ep_plan, on the GPU): one block
+// reads the all-gathered count matrix and writes the scatter routes, the
+// epilogue routes and the receive plan (counts, offsets, 128-row tile table),
+// so an expert-parallel step needs no host synchronisation at all.
+__global__ void ep_layout_kernel(const int32_t* __restrict__ cnt, int W, int el, int align, int r,
+                                 int32_t* __restrict__ g_rank, int64_t* __restrict__ g_delta,
+                                 int32_t* __restrict__ rt, int32_t* __restrict__ rcounts,
+                                 int32_t* __restrict__ roffsets, int32_t* __restrict__ tile_expert,
+                                 int32_t* __restrict__ n_tiles) {
+  extern __shared__ int32_t sm[];
+  const int E = W * el, C = el * W;
+  int32_t* send_off = sm;          // [W][E]
+  int32_t* chunk = sm + W * E;     // [W][el*W]: chunk_off of every rank p
+  int32_t* boff = chunk + W * C;   // [el+1]: my block offsets
+  for (int s = threadIdx.x; s < W; s += blockDim.x) {  // send_section_offsets, collectives.cpp:114-122
+    int acc = 0;
+    for (int g = 0; g < E; ++g) {
+      send_off[s * E + g] = acc;
+      acc += cnt[s * E + g];
+    }
+  }
+  for (int p = threadIdx.x; p < W; p += blockDim.x) {  // recv_chunk_offsets, collectives.cpp:126-135
+    int at = 0;
+    for (int e = 0; e < el; ++e) {
+      int c = at;
+      for (int s = 0; s < W; ++s) {
+        chunk[p * C + e * W + s] = c;
+        c += cnt[s * E + p * el + e];
+      }
+      const int rows = c - at;
+      if (p == r) {
+        rcounts[e] = rows;
+        boff[e] = at;
+      }
+      at += (rows + align - 1) / align * align;
+    }
+    if (p == r) boff[el] = at;
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < E; g += blockDim.x) {
+    const int p = g / el, e = g % el;
+    g_rank[g] = p;
+    g_delta[g] = (int64_t)chunk[p * C + e * W + r] - send_off[r * E + g];
+  }
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const int e = c / W, s = c % W;
+    rt[c] = chunk[r * C + c];
+    rt[C + c] = cnt[s * E + r * el + e];
+    rt[2 * C + c] = send_off[s * E + r * el + e];
+  }
+  for (int e = threadIdx.x; e <= el; e += blockDim.x) roffsets[e] = boff[e];
+  for (int e = 0; e < el; ++e)
+    for (int t = boff[e] / 128 + threadIdx.x; t < boff[e + 1] / 128; t += blockDim.x) tile_expert[t] = e;
+  if (threadIdx.x == 0) *n_tiles = boff[el] / 128;
+}
+
+// Zero the pad rows of every expert block of the receive layout (device
+// offsets / counts): block e, one warp per row, 16-byte stores.
+__global__ void ep_zero_pads_kernel(uint8_t* __restrict__ buf, int64_t row_bytes, const int32_t* __restrict__ offsets,
+                                    const int32_t* __restrict__ counts) {
+  const int e = blockIdx.x;
+  const int64_t a = (int64_t)offsets[e] + counts[e], z = offsets[e + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t row = a + warp; row < z; row += blockDim.x >> 5) {
+    uint4* d = reinterpret_cast<uint4*>(buf + row * row_bytes);
+    for (int64_t c = lane; c < (row_bytes >> 4); c += 32) d[c] = make_uint4(0, 0, 0, 0);
+  }
+}
+
+static size_t ep_layout_smem(int W, int64_t el) {
+  const int64_t E = W * el;
+  return (size_t)(W * E + W * el * W + el + 1) * 4;
+}
+
+// Fused-path plan with no host synchronisation: counts all-gathered over
+// peer memory, every layout computed on the device.
+static void ep_plan_peer_device(Layer& L) {
+  Ctx* ctx = L.ctx;
+  Layer::Ep& P = *L.ep;
+  const int W = P.W;
+  const int64_t el = P.el, E = L.E, C = el * W;
+  P.peer.put_counts(ctx, L.plan.counts, E);
+  P.peer.wait(ctx, PH_COUNTS);
+  ep_layout_kernel<<<1, 256, ep_layout_smem(W, el), ctx->stream>>>(
+      P.cnt_mat, W, (int)el, (int)P.align, P.r, P.g_rank, P.g_delta, P.rt, P.rplan.counts, P.rplan.offsets,
+      P.rplan.tile_expert, P.rplan.n_tiles);
+  CK_LAUNCH(ctx);
+  (void)C;
+  P.planned = true;
+}
+
+static void ep_zero_pads_device(Ctx* ctx, const Layer::Ep& P, size_t rb, void* buf) {
+  if (P.el == 0 || P.align <= 1) return;
+  ep_zero_pads_kernel<<<(unsigned)P.el, 256, 0, ctx->stream>>>(static_cast<uint8_t*>(buf), (int64_t)rb,
+                                                                P.rplan.offsets, P.rplan.counts);
+  CK_LAUNCH(ctx);
+}
+
 // Count all-gather over peer memory (exchange_counts, collectives.cpp:69-109:
 // every rank receives every rank's full count vector), the one host sync of
 // an EP step, then the layouts of ALL ranks: this rank's receive layout (as
@@ -378,9 +478,15 @@ void Layer::ep_forward(const void* x, void* y) {
     // fused: scatter straight into the expert ranks (global_scatter), fc2
     // epilogue straight back into the source ranks (global_gather)
     P.peer.epoch++;
-    ep_plan_peer(*this);                       // C1 + every rank's layout
+    P.device_plan = ep_layout_smem(P.W, P.el) <= 48 * 1024 && P.align % 16 == 0 && rb % 16 == 0;
+    if (P.device_plan) {
+      ep_plan_peer_device(*this);              // C1 + layouts on the device: no host sync
+      ep_zero_pads_device(ctx, P, rb, P.xs);
+    } else {
+      ep_plan_peer(*this);                     // C1 + every rank's layout on the host
+      zero_pads(ctx, P, rb, P.xs);
+    }
     ctx_mark(ctx, MARK_PLAN);
-    zero_pads(ctx, P, rb, P.xs);
     ScatterRoute sr{idx, P.g_rank, P.g_delta, P.peer.d_ptr[PB_XS]};
     scatter(ctx, t, x, d, plan, nullptr, &sr);  // C2 fused
     P.peer.signal(ctx, PH_SCATTER);
@@ -419,7 +525,10 @@ void Layer::ep_backward(const void* dy, void* dx) {
     // gradients ride the same routes: d_ys straight into the expert ranks,
     // the dgrad-fc1 epilogue straight back into the source ranks; the weight
     // gradients and the gate's d_wg run while the peers finish
-    zero_pads(ctx, P, rb, P.d_ys);
+    if (P.device_plan)
+      ep_zero_pads_device(ctx, P, rb, P.d_ys);
+    else
+      zero_pads(ctx, P, rb, P.d_ys);
     ScatterRoute sr{idx, P.g_rank, P.g_delta, P.peer.d_ptr[PB_DYS]};
     gather_combine_bwd(ctx, t, dy, ys, d, plan, vals, nullptr, d_w, gate ? scores : nullptr,
                        gate ? idx : nullptr, gate ? dz_bf16 : nullptr, &sr);

@@ -385,8 +385,12 @@ __device__ __forceinline__ void drain_bf16(const Params& p, const Tile& tl, cons
       uint32_t bits = 0;
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        v[j] = fmaxf(v[j], 0.f);  // v >= +0 afterwards: v > 0 <=> its bits are nonzero
-        bits |= ((__float_as_uint(v[j]) + 0x7FFFFFFFu) >> 31) << j;
+        // relu on the bit pattern: every negative float (-0 included) is a
+        // negative int, so max(bits, 0) is +0 for them and v otherwise; the
+        // mask bit is min(bits, 1) (v > 0 <=> nonzero bits)
+        const int xi = max(__float_as_int(v[j]), 0);
+        v[j] = __int_as_float(xi);
+        bits += min((uint32_t)xi, 1u) << j;
       }
       if (p.relu_bits_out) p.relu_bits_out[relu_bits_index(row, tl.n0 + c * 32, p.N)] = bits;
     }
