@@ -299,19 +299,21 @@ def run_ours(args, world, rank, cfg):
         if dist:
             dist.barrier()
         launches0 = ctx.launches
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         torch.cuda.synchronize()
-        t0.record(stream)
-        for _ in range(args.steps):
+        evs[0].record(stream)
+        for i in range(args.steps):
             step()
-        t1.record(stream)
+            evs[i + 1].record(stream)
         torch.cuda.synchronize()
         clk = clocks.stop()
+        t0, t1 = evs[0], evs[-1]
+        per_step = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
         if dist:
             dist.barrier()
         launches = ctx.launches - launches0
         ms = t0.elapsed_time(t1) / args.steps
+        ms_sd = statistics.stdev(per_step) if len(per_step) > 1 else 0.0
         stage = (C.c_float * len(STAGES))()
         done = C.c_int()
         _lib.check(_lib.lib.fmoe_ctx_profile_read(ctx.h, stage, len(STAGES), C.byref(done)))
@@ -373,8 +375,8 @@ def run_ours(args, world, rank, cfg):
     gather_bytes = s * d * (n * k + n) + 8 * n * k
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16",
+        "warmup": args.warmup, "ms_per_step": ms, "ms_per_step_stddev": ms_sd, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (uniform[-1,1) inputs; reference init_state weights"
                 + ("; injected Zipf routing" if wl == "cfg5" else "") + ")",
         "config": {"workload": workload_name(wl, cfg, world), "n_b_per_gpu": n, "d_m": d, "d_h": h,

@@ -164,6 +164,50 @@ __global__ void scatter_bwd_kernel(const T* __restrict__ d_xs, int64_t d, fmoe_p
   const int lane = threadIdx.x & 31;
   if (i >= p.n_b) return;
   const int k = (int)p.k;
+  if ((d % V) == 0 && k <= 4) {
+    // every slot's rows (and the addend) in flight together; adds in slot
+    // order then the addend, as below
+    constexpr int U = 4;
+    const int64_t nv = d / V;
+    const T* src[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) src[j] = j < k ? d_xs + (int64_t)__ldg(p.inverse_pos + i * k + j) * d : d_xs;
+    for (int64_t c0 = lane; c0 < nv; c0 += 32 * U) {
+      uint4 raw[4][U], ad[U];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (j < k && c0 + 32 * u < nv) raw[j][u] = __ldg(reinterpret_cast<const uint4*>(src[j]) + c0 + 32 * u);
+      if (addend)
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (c0 + 32 * u < nv) ad[u] = __ldg(reinterpret_cast<const uint4*>(addend + i * d) + c0 + 32 * u);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (c0 + 32 * u >= nv) continue;
+        A acc[V];
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc[e] = A(0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (j >= k) break;
+          A g[V];
+          unpack16<T, A>(raw[j][u], g);
+#pragma unroll
+          for (int e = 0; e < V; ++e) acc[e] += g[e];
+        }
+        if (addend) {
+          A g[V];
+          unpack16<T, A>(ad[u], g);
+#pragma unroll
+          for (int e = 0; e < V; ++e) acc[e] += g[e];
+        }
+        reinterpret_cast<uint4*>(dx + i * d)[c0 + 32 * u] = pack16<T, A>(acc);
+      }
+    }
+    return;
+  }
   if ((d % V) == 0) {
     const int64_t nv = d / V;
 #pragma unroll 4
@@ -229,11 +273,85 @@ __global__ void gcb_kernel(const T* __restrict__ dy, const T* __restrict__ ys, i
     if (p.align <= 1) return;
     const int64_t row = pad_row(p, i - p.n_b);
     if (row < 0) return;
-    for (int64_t c = lane; c < d; c += 32) d_ys[row * d + c] = T(0);
+    if ((d % V) == 0) {
+      uint4* d4 = reinterpret_cast<uint4*>(d_ys + row * d);
+      for (int64_t c = lane; c < d / V; c += 32) d4[c] = make_uint4(0, 0, 0, 0);
+    } else {
+      for (int64_t c = lane; c < d; c += 32) d_ys[row * d + c] = T(0);
+    }
     return;
   }
   const T* dyr = dy + i * d;
   float dw_f[8];
+  if constexpr (!std::is_same<T, double>::value) {
+    if ((d % V) == 0 && k <= 2) {
+      // fp32-accumulating fast path: the token's d_y slice is loaded once and
+      // every slot's ys loads are in flight together (same per-lane order of
+      // the dot products as the generic loop below, so the same bits)
+      constexpr int U = 4;
+      const int64_t nv = d / V;
+      T* dr[2];
+      const T* yr[2];
+      A wt[2], part[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        if (j >= k) {
+          dr[j] = d_ys;
+          yr[j] = ys;
+          wt[j] = A(0);
+          part[j] = A(0);
+          continue;
+        }
+        const int64_t pos = __ldg(p.inverse_pos + i * k + j);
+        wt[j] = (A)__ldg(w + i * k + j);
+        dr[j] = d_ys + pos * d;
+        if (route.idx) {
+          const int g = __ldg(route.idx + i * k + j);
+          dr[j] = reinterpret_cast<T*>(route.dst[__ldg(route.g_rank + g)]) + (pos + __ldg(route.g_delta + g)) * d;
+        }
+        yr[j] = ys + pos * d;
+        part[j] = A(0);
+      }
+      for (int64_t c0 = lane; c0 < nv; c0 += 32 * U) {
+        uint4 gv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (c0 + 32 * u < nv) gv[u] = __ldg(reinterpret_cast<const uint4*>(dyr) + c0 + 32 * u);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          if (j >= k) break;
+          uint4 yv4[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (c0 + 32 * u < nv) yv4[u] = __ldg(reinterpret_cast<const uint4*>(yr[j]) + c0 + 32 * u);
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (c0 + 32 * u < nv) {
+              A g[V], yv[V], o[V];
+              unpack16<T, A>(gv[u], g);
+              unpack16<T, A>(yv4[u], yv);
+#pragma unroll
+              for (int e = 0; e < V; ++e) {
+                o[e] = wt[j] * g[e];
+                part[j] = fma(g[e], yv[e], part[j]);
+              }
+              reinterpret_cast<uint4*>(dr[j])[c0 + 32 * u] = pack16<T, A>(o);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        if (j >= k) break;
+        A dot = part[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        if (lane == 0) d_w[i * k + j] = (S)dot;
+        dw_f[j] = (float)dot;
+      }
+      goto gate_jacobian;
+    }
+  }
   for (int j = 0; j < k; ++j) {
     const int64_t pos = __ldg(p.inverse_pos + i * k + j);
     const A wt = (A)__ldg(w + i * k + j);
@@ -282,6 +400,7 @@ __global__ void gcb_kernel(const T* __restrict__ dy, const T* __restrict__ ys, i
     if (lane == 0) d_w[i * k + j] = (S)dot;
     if (j < 8) dw_f[j] = (float)dot;
   }
+gate_jacobian:
   if (dz != nullptr) {
     // Softmax Jacobian (gate.cpp:44-59) fused: ds is k-sparse.
     const int E = (int)p.n_experts;

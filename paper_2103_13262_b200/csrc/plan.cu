@@ -36,15 +36,20 @@ __global__ void plan_hist(const int32_t* __restrict__ idx, int64_t nk, int n_exp
   const int64_t chunk = (int64_t)blockIdx.x * kWarpsPerCta + w;
   const int64_t f0 = chunk * kChunk;
   if (f0 < nk) {
-    for (int s = 0; s < kChunk; s += 32) {
-      const int64_t f = f0 + s + lane;
-      int key = -1;
-      if (f < nk) {
-        key = __ldg(idx + f);
-        if (key < 0 || key >= n_experts) {
-          atomicExch(err, 1);
-          key = -1;
-        }
+    // all of the lane's keys in flight at once (the loop below is latency-bound otherwise)
+    int keys[kChunk / 32];
+#pragma unroll
+    for (int t = 0; t < kChunk / 32; ++t) {
+      const int64_t f = f0 + t * 32 + lane;
+      keys[t] = f < nk ? __ldg(idx + f) : -1;
+    }
+#pragma unroll
+    for (int t = 0; t < kChunk / 32; ++t) {
+      const int64_t f = f0 + t * 32 + lane;
+      int key = keys[t];
+      if (f < nk && (key < 0 || key >= n_experts)) {
+        atomicExch(err, 1);
+        key = -1;
       }
       const unsigned peers = __match_any_sync(0xffffffffu, key);
       if (key >= 0 && (__ffs(peers) - 1) == lane) hist[key] += __popc(peers);
@@ -148,19 +153,28 @@ __global__ void plan_rank(const int32_t* __restrict__ idx, int64_t nk, int k, in
   if (f0 >= nk) return;
   const int32_t* base = chunk_base + chunk;  // base[key * n_chunks]
   const unsigned lt = (1u << lane) - 1u;
-  for (int s = 0; s < kChunk; s += 32) {
-    const int64_t f = f0 + s + lane;
-    int key = -1;
-    if (f < nk) {
-      key = __ldg(idx + f);
-      if (key < 0 || key >= n_experts) key = -1;
-    }
+  int keys[kChunk / 32];
+#pragma unroll
+  for (int t = 0; t < kChunk / 32; ++t) {
+    const int64_t f = f0 + t * 32 + lane;
+    keys[t] = f < nk ? __ldg(idx + f) : -1;
+  }
+  int bases[kChunk / 32];  // the chunk base of every key, loads in flight together
+#pragma unroll
+  for (int t = 0; t < kChunk / 32; ++t) {
+    if (keys[t] >= n_experts || keys[t] < 0) keys[t] = -1;
+    bases[t] = keys[t] >= 0 ? __ldg(base + (int64_t)keys[t] * n_chunks) : 0;
+  }
+#pragma unroll
+  for (int t = 0; t < kChunk / 32; ++t) {
+    const int64_t f = f0 + t * 32 + lane;
+    const int key = keys[t];
     const unsigned peers = __match_any_sync(0xffffffffu, key);
     int before = 0;
     if (key >= 0) before = run[key];
     __syncwarp();
     if (key >= 0) {
-      const int pos = __ldg(base + (int64_t)key * n_chunks) + before + __popc(peers & lt);
+      const int pos = bases[t] + before + __popc(peers & lt);
       const int i = (int)(f / k);
       src_row[pos] = i;
       slot[pos] = (int)(f - (int64_t)i * k);

@@ -269,6 +269,113 @@ __device__ __forceinline__ void load_chunk(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Gate epilogue for E <= 64 (BN = 64): the row's logits stay in registers, so
+// each exp is computed once; scores leave as 16-byte stores; top-2 (the
+// common case) is a two-slot insertion.  Same arithmetic as epi_gate below:
+// max, exp(l - max), sequential sum, correctly rounded division, descending
+// selection with ties to the lower expert (matrix.cpp:155-189).
+__device__ __forceinline__ void epi_gate64(const Params& p, uint32_t tbase, int row) {
+  const int E = p.N;
+  float ev[64];
+  {
+    uint32_t r0[32], r1[32];
+    tmem_ld_issue(tbase, r0);
+    if (E > 32) tmem_ld_issue(tbase + 32, r1);
+    tmem_ld_wait(r0);
+    if (E > 32) tmem_ld_wait(r1);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      ev[i] = __uint_as_float(r0[i]);
+      ev[32 + i] = E > 32 ? __uint_as_float(r1[i]) : 0.f;
+    }
+  }
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < 64; ++i)
+    if (i < E) mx = fmaxf(mx, ev[i]);
+  float sum = 0.f;
+#pragma unroll
+  for (int i = 0; i < 64; ++i)
+    if (i < E) {
+      ev[i] = expf(ev[i] - mx);
+      sum += ev[i];
+    }
+#pragma unroll
+  for (int i = 0; i < 64; ++i) ev[i] = __fdiv_rn(ev[i], sum);
+  const bool valid = row < p.M;
+  const int k = p.topk;
+  if (valid) {
+    float* srow = p.scores + (int64_t)row * E;
+    if (E == 64) {
+#pragma unroll
+      for (int i = 0; i < 64; i += 4)
+        *reinterpret_cast<float4*>(srow + i) = make_float4(ev[i], ev[i + 1], ev[i + 2], ev[i + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 64; ++i)
+        if (i < E) srow[i] = ev[i];
+    }
+  }
+  if (!valid || k <= 0) return;
+  if (k == 2) {
+    float v0 = -INFINITY, v1 = -INFINITY;
+    int i0 = -1, i1 = -1;
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      if (i < E) {
+        const float s = ev[i];
+        if (s > v0) {
+          v1 = v0; i1 = i0; v0 = s; i0 = i;
+        } else if (s > v1) {
+          v1 = s; i1 = i;
+        }
+      }
+    }
+    p.topk_idx[(int64_t)row * 2] = i0;
+    p.topk_idx[(int64_t)row * 2 + 1] = i1;
+    p.topk_val[(int64_t)row * 2] = v0;
+    p.topk_val[(int64_t)row * 2 + 1] = v1;
+    return;
+  }
+  constexpr int KMAX = 8;
+  float tv[KMAX];
+  int ti[KMAX];
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j) {
+    tv[j] = -INFINITY;
+    ti[j] = -1;
+  }
+#pragma unroll
+  for (int i = 0; i < 64; ++i) {
+    if (i < E) {
+      float cs = ev[i];
+      int ci = i;
+      bool carry = false;
+#pragma unroll
+      for (int j = 0; j < KMAX; ++j) {
+        if (j < k) {
+          const bool take = carry || (cs > tv[j]);
+          if (take) {
+            const float tf = tv[j];
+            const int tix = ti[j];
+            tv[j] = cs;
+            ti[j] = ci;
+            cs = tf;
+            ci = tix;
+            carry = true;
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j)
+    if (j < k) {
+      p.topk_idx[(int64_t)row * k + j] = ti[j];
+      p.topk_val[(int64_t)row * k + j] = tv[j];
+    }
+}
+
 // Gate epilogue: the thread owns one token row and all E = N logits.
 // softmax_rows (matrix.cpp:155-170): max, exp(l - max), sequential sum, divide;
 // topk_rows (matrix.cpp:172-189): descending, ties keep the lower expert.
@@ -462,7 +569,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(tfull + a), 1);
-      mbar_init(smem_u32(tempty + a), 8 * CG);  // one arrive per epilogue warp of the pair
+      // one arrive per epilogue warp of the pair (the gate epilogue's two warp
+      // groups take alternate tiles: 4 arrivals)
+      mbar_init(smem_u32(tempty + a), (EPI == EPI_GATE ? 4 : 8) * CG);
     }
     fence_mbarrier_init();
   }
@@ -598,11 +707,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         continue;
       }
+      if constexpr (EPI == EPI_GATE) {
+        // one thread owns a whole row of logits; the two warp groups drain
+        // alternate tiles (accumulators) so two tiles' softmax run at once
+        if ((ew >> 2) == acc) {
+          mbar_wait(smem_u32(tfull + acc), acc_phase);
+          tc_fence_after();
+          const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+          if constexpr (BN == 64)
+            epi_gate64(p, tb, row);
+          else
+            epi_gate<BN>(p, tb, row);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(tempty + acc));
+        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        continue;
+      }
       mbar_wait(smem_u32(tfull + acc), acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       if constexpr (EPI == EPI_GATE) {
-        if (ew < 4) epi_gate<BN>(p, tbase, row);  // one thread owns a whole row of logits
       } else if (EPI == EPI_GATE_DX && p.gk <= 2) {
         // scatter_backward gather fused with the gate d_x: the row's k source
         // positions are read once per tile and both source rows of a chunk are
