@@ -18,20 +18,22 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;             // two fp32 accumulators
   static constexpr int COLSUM_BYTES = 4 * BN * 4;      // per-warp column sums of one tile
-  // outputs leave through TMA stores from (32 rows x 32 columns) staging
-  // tiles per epilogue warp: bf16 rows of 64 B (64B swizzle, double-buffered),
-  // fp32 rows of 128 B (128B swizzle, single buffer)
+  // outputs leave through TMA stores from per-warp staging tiles of 32 rows x
+  // 64 B (64B swizzle): 32 bf16 columns, or 16 fp32 columns (a 32-column fp32
+  // chunk is stored as two halves).  One tile per warp keeps 6 pipeline
+  // stages in shared memory.
   static constexpr bool TMA_STORE = EPI == EPI_BF16 || EPI == EPI_MASK_BF16 || EPI == EPI_F32;
-  static constexpr int OUT_ROW_BYTES = EPI == EPI_F32 ? 128 : 64;
-  static constexpr int NBUF = EPI == EPI_F32 ? 1 : 2;
+  static constexpr int OUT_ROW_BYTES = 64;
+  static constexpr int NBUF = 1;
   static constexpr int TILE_BYTES = 32 * OUT_ROW_BYTES;
   static constexpr int STORE_BYTES = TMA_STORE ? 8 * NBUF * TILE_BYTES : 0;
   // bf16 epilogues stage the bias of each warp's 128-column slice of the tile
   static constexpr int BIAS_BYTES = EPI == EPI_BF16 ? 8 * (BN / 2) * 4 : 0;
-  static constexpr int BUDGET = 200 * 1024 - STORE_BYTES - COLSUM_BYTES - BIAS_BYTES;
+  static constexpr int BUDGET = 224 * 1024 - STORE_BYTES - COLSUM_BYTES - BIAS_BYTES;
   static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
   static constexpr int SMEM =
       STAGES * STAGE_BYTES + STORE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + COLSUM_BYTES + BIAS_BYTES;
+  static_assert(SMEM <= 227 * 1024, "tc_gemm: shared memory over the sm_100 per-CTA limit");
 };
 
 // Named barrier among the 4 epilogue warps (ids 1.. are free; 0 = __syncthreads).
@@ -138,23 +140,6 @@ __device__ __forceinline__ void epi_store_chunk(const Params& p, const Tile& tl,
                                                 uint32_t stage_addr = 0) {
   // row: absolute row in the output tile space; c0: absolute column of v[0]
   if constexpr (EPI == EPI_F32) {
-    if (stage_addr) {
-      // 32 rows x 128 B staging tile, TMA SWIZZLE_128B layout: 16-byte chunk j
-      // of row r at r*128 + ((j ^ (r & 7)) << 4); rows >= M are clipped or
-      // never stored (tiles do not cross groups when TMA stores are enabled)
-      const uint32_t r = threadIdx.x & 31;
-      const uint32_t base = stage_addr + r * 128;
-      const bool live = row < p.M;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t a = base + (((uint32_t)j ^ (r & 7u)) << 4);
-        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(live ? v[4 * j] : 0.f),
-                     "f"(live ? v[4 * j + 1] : 0.f), "f"(live ? v[4 * j + 2] : 0.f),
-                     "f"(live ? v[4 * j + 3] : 0.f)
-                     : "memory");
-      }
-      return;
-    }
     float* out = reinterpret_cast<float*>(p.C) + (int64_t)tl.g * p.c_group_stride +
                  (int64_t)row * p.ldc + c0;
     if (row >= p.M) return;
@@ -837,6 +822,38 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             float v[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(buf[i & 1][j]);
+            if constexpr (EPI == EPI_F32) {
+              if (p.tma_out) {
+                // two 16-column halves through the warp's 32 x 64 B staging tile
+                // (64B swizzle: 16-byte chunk j of row r at r*64 + ((j ^ ((r >> 1) & 3)) << 4));
+                // rows >= M are staged as zeros and clipped by the tensor map
+                const int out_row = (p.c_group_stride ? tl.g * (int)(p.c_group_stride / p.ldc) : 0) + tl.m0 +
+                                    row_off + q * 32;
+                const uint32_t stage = smem_u32(sOut) + (uint32_t)(ew * C::TILE_BYTES);
+                const uint32_t r = (uint32_t)lane;
+                const bool live = row < p.M;
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                  if (lane == 0) bulk_wait_read<0>();
+                  __syncwarp();
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) {
+                    const uint32_t a = stage + r * 64 + (((uint32_t)j ^ ((r >> 1) & 3u)) << 4);
+                    const float* src = v + hh * 16 + 4 * j;
+                    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(live ? src[0] : 0.f),
+                                 "f"(live ? src[1] : 0.f), "f"(live ? src[2] : 0.f), "f"(live ? src[3] : 0.f)
+                                 : "memory");
+                  }
+                  fence_proxy_async_smem();
+                  __syncwarp();
+                  if (lane == 0) {
+                    tma_store_2d(&tmC, stage, tl.n0 + c * 32 + hh * 16, out_row);
+                    bulk_commit();
+                  }
+                }
+                continue;
+              }
+            }
             uint32_t stage = 0;
             if (C::TMA_STORE && p.tma_out) {  // reuse a staging tile only once its last TMA store read it
               stage = smem_u32(sOut) + (uint32_t)((ew * C::NBUF + sbuf) * C::TILE_BYTES);
@@ -962,7 +979,7 @@ static void launch_t(Ctx* ctx, const CUtensorMap& ta, const CUtensorMap& tb, con
                       (!grouped || (p.M % (BM * CG) == 0 && p.c_group_stride == (int64_t)p.M * p.ldc));
       if (ok) {
         const int64_t rows = grouped ? (int64_t)p.M * p.n_groups : p.M;
-        tc_out = make_tmap(p.C, p.N, rows, p.ldc * 4, 32, 32, 128, true);
+        tc_out = make_tmap(p.C, p.N, rows, p.ldc * 4, 16, 32, 64, true);
         q.tma_out = 1;
       }
     } else if (!p.route_out) {
