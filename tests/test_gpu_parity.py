@@ -411,3 +411,53 @@ def test_dense_primitives_compose_to_the_gate(fm, dtype):
         fm.topk_rows(s, 25)
     with pytest.raises(fm.ShapeError):
         fm.matmul(x, x)
+
+
+# ----------------------------------------------- full-size properties (cfg2)
+def test_permutes_full_size_round_trips(fm):
+    """BASELINE cfg2 size (65536 tokens, d=1024, 64 experts, top-2, 256-row
+    blocks): size-independent identities that hold bit for bit --
+    scatter_backward(scatter(x)) == k*x and gather_combine(scatter(x), 1/k) == x
+    (halving, doubling and the two-term sums are exact in fp32 and bf16)."""
+    n, d, e, k = 65536, 1024, 64, 2
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    x = (torch.rand(n, d, device="cuda", generator=g) * 2 - 1).bfloat16()
+    first = torch.randint(0, e, (n, 1), device="cuda", generator=g)
+    step = torch.randint(1, e, (n, 1), device="cuda", generator=g)
+    idx = torch.cat([first, (first + step) % e], dim=1)  # two distinct experts per token
+    p = fm.build_plan(idx.int(), e, align=256)
+    xs = fm.scatter(x, p)
+    assert torch.equal(fm.scatter_backward(xs, p), x * 2)
+    half = torch.full((n, k), 0.5, device="cuda")
+    assert torch.equal(fm.gather_combine(xs, p, half), x)
+    counts = p.counts.cpu().long()
+    assert int(counts.sum()) == n * k and (host(p.offsets) % 256 == 0).all()
+
+
+# --------------------------------------------------------- fp32 layer (§8c)
+def test_layer_f32_vs_oracle(fm, orc):
+    """FMOE_F32 (SIMT fp32) against the oracle fed the same fp32 values:
+    outputs max-abs-err <= 1e-5 * max|ref|, gradients rel-L2 <= 1e-4 (SURVEY
+    §8c parity protocol (3)), routing exact on well-separated tokens."""
+    n, d, h, e, k, seed = 512, 64, 128, 8, 2, 21
+    layer = fm.MoELayer(fm.MoEConfig(n, d, h, k, e, 1, seed), dtype=torch.float32)
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)  # noqa: E731
+    x = f32(orc.seeded_matrix(seed, 102, n, d))
+    dy = f32(orc.seeded_matrix(seed, 103, n, d))
+    y = layer.forward(dev(x, torch.float32))
+    dx = layer.backward(dev(dy, torch.float32))
+    torch.cuda.synchronize()
+    w = dict(wg=host(layer.w_g), w1=host(layer.experts.w1), b1=host(layer.experts.b1), w2=host(layer.experts.w2),
+             b2=host(layer.experts.b2))
+    o = orc.moe_forward_backward(x, dy, k, **w)
+    idx = host(layer.routing()[0]).astype(np.int64)
+    ok = well_separated_rows(o["scores"], k)
+    assert np.array_equal(idx[ok], o["idx"][ok])
+    same = (idx == o["idx"]).all(axis=1)
+    assert same.all()
+    assert np.abs(host(y) - o["y"]).max() <= 1e-5 * np.abs(o["y"]).max()
+    assert rel_l2(host(dx), o["dx"]) <= 1e-4
+    for a, key in ((layer.d_wg, "dwg"), (layer.grads.d_w1, "dw1"), (layer.grads.d_b1, "db1"),
+                   (layer.grads.d_w2, "dw2"), (layer.grads.d_b2, "db2")):
+        assert rel_l2(host(a), o[key]) <= 1e-4, key
