@@ -329,11 +329,18 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     tc::launch(ctx, 256, false, false, ta, tb, p, max_tiles * ceil_div(h, 256), cg);
     ctx_mark(ctx, MARK_DGRAD2);
   }
+  // weight-gradient tiles heaviest expert first (skewed routing)
+  int* group_order = nullptr;
+  if (do_wgrad) {
+    group_order = reinterpret_cast<int*>(part_ws + (cap / 128 + 1) * (d + h));
+    order_groups_desc(ctx, b.offsets, E, group_order);
+  }
   if (do_wgrad) {  // wgrad fc2: d_w2[e] = hidden_e^T d_ys_e  (M = h, N = d, K = rows of e)
     const CUtensorMap ta = tc::make_tmap(hidden, h, cap, h * 2, 64, 64);
     const CUtensorMap tb = tc::make_tmap(d_ys, d, cap, d * 2, 64, 64);
     tc::Params p{};
     p.mode = tc::RAGGED_K; p.M = (int)h; p.N = (int)d; p.n_groups = (int)E; p.k_offsets = b.offsets;
+    p.group_order = group_order;
     p.epi = tc::EPI_F32; p.C = g.d_w2; p.ldc = d; p.c_group_stride = h * d;
     tc::launch(ctx, 256, true, true, ta, tb, p, E * ceil_div(h, 128 * cg) * ceil_div(d, 256), cg);
     ctx_mark(ctx, MARK_WGRAD2);
@@ -361,6 +368,7 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     const CUtensorMap tb = tc::make_tmap(d_pre, h, cap, h * 2, 64, 64);
     tc::Params p{};
     p.mode = tc::RAGGED_K; p.M = (int)d; p.N = (int)h; p.n_groups = (int)E; p.k_offsets = b.offsets;
+    p.group_order = group_order;
     p.epi = tc::EPI_F32; p.C = g.d_w1; p.ldc = h; p.c_group_stride = d * h;
     tc::launch(ctx, 256, true, true, ta, tb, p, E * ceil_div(d, 128 * cg) * ceil_div(h, 256), cg);
     ctx_mark(ctx, MARK_WGRAD1);
@@ -372,7 +380,8 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
 }
 
 int64_t experts_bwd_part_floats(const fmoe_plan& b, int64_t d, int64_t h) {
-  return (b.capacity / 128 + 1) * (d + h);
+  // bias-gradient tile partials, then the weight-gradient group order (ints)
+  return (b.capacity / 128 + 1) * (d + h) + b.n_experts + 64;
 }
 
 }  // namespace fmoe_b200

@@ -477,7 +477,27 @@ __global__ void reduce_tile_partials_kernel(const float* __restrict__ part, int6
   out[(int64_t)e * n_cols + c] = s;
 }
 
+// order[rank] = group, ranked by decreasing row count (offsets[g+1] -
+// offsets[g]), ties by index: O(G^2) comparisons in one block.
+__global__ void order_groups_kernel(const int32_t* __restrict__ offsets, int G, int32_t* __restrict__ order) {
+  for (int g = threadIdx.x; g < G; g += blockDim.x) {
+    const int c = offsets[g + 1] - offsets[g];
+    int rank = 0;
+    for (int h = 0; h < G; ++h) {
+      const int ch = offsets[h + 1] - offsets[h];
+      rank += (ch > c) || (ch == c && h < g);
+    }
+    order[rank] = g;
+  }
+}
+
 }  // namespace
+
+void order_groups_desc(Ctx* ctx, const int32_t* offsets, int64_t groups, int32_t* order) {
+  if (groups <= 0) return;
+  order_groups_kernel<<<1, 1024, 0, ctx->stream>>>(offsets, (int)groups, order);
+  CK_LAUNCH(ctx);
+}
 
 void tile_colsum(Ctx* ctx, const __nv_bfloat16* src, int64_t n_cols, const int32_t* n_tiles,
                  int64_t max_tiles, float* part) {

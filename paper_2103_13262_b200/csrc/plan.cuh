@@ -26,6 +26,8 @@ void gather_combine_bwd(Ctx* ctx, fmoe_dtype t, const void* dy, const void* ys, 
                         const fmoe_plan& p, const void* w, void* d_ys, void* d_w,
                         const void* scores, const int32_t* topk_idx, __nv_bfloat16* dz,
                         const ScatterRoute* route = nullptr);
+// order[r] = the group of rank r by decreasing row count (ties by index).
+void order_groups_desc(Ctx* ctx, const int32_t* offsets, int64_t groups, int32_t* order);
 // Bias gradients: out[g][c] = sum over the rows of block g (ascending) of src[row][c].
 void block_colsum(Ctx* ctx, fmoe_dtype t, const void* src, int64_t n_cols, const int32_t* offsets,
                   const int32_t* counts, int64_t n_blocks, void* out);

@@ -55,6 +55,10 @@ struct Params {
   const int* tile_group;     // RAGGED_M: group of each 128-row tile (NULL: all group 0)
   const int* n_mtiles;       // RAGGED_M: device count of valid row tiles (NULL: ceil(M/128))
   const int* k_offsets;      // RAGGED_K: [G+1] K-row range of each group (multiples of 64)
+  // RAGGED_K (optional): groups in decreasing K-length; tiles are then dealt
+  // to the persistent CTAs heaviest first in a snake (boustrophedon) order so
+  // skewed expert sizes (Zipf routing) stay balanced across SMs
+  const int* group_order;
   int b_group_rows;          // RAGGED_M: rows of the 2-D B tensor per group
   // epilogue
   int epi;
