@@ -16,6 +16,8 @@
 //                    pos(f) = base[c][e] + #{f' < f in chunk c : idx[f'] = e},
 //                    exactly the reference's row-major fill order.
 // Integer-exact by construction; checked bit-for-bit against the oracle.
+#include <mutex>
+
 #include "common.cuh"
 #include "plan.cuh"
 
@@ -208,13 +210,12 @@ void plan_build(Ctx* ctx, const int32_t* topk_idx, const fmoe_plan& p) {
   const int64_t chunks = ceil_div(nk, kChunk);
   int32_t* chunk_hist = reinterpret_cast<int32_t*>(p.scratch);
   const size_t smem = (size_t)E * kWarpsPerCta * 4;
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag attr_once[64];  // function attributes are per device
+  std::call_once(attr_once[ctx->device & 63], [] {
     CK(cudaFuncSetAttribute(plan_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CK(cudaFuncSetAttribute(plan_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CK(cudaFuncSetAttribute(plan_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  });
   const unsigned grid = (unsigned)std::max<int64_t>(1, ceil_div(chunks, kWarpsPerCta));
   if (nk > 0) {
     plan_hist<<<grid, 32 * kWarpsPerCta, smem, ctx->stream>>>(topk_idx, nk, E, (int)chunks, chunk_hist,

@@ -1003,8 +1003,8 @@ static void launch_t(Ctx* ctx, const CUtensorMap& ta, const CUtensorMap& tb, con
       q.tma_out = 1;
     }
   }
-  static std::once_flag attr_once[8];
-  std::call_once(attr_once[ctx->device & 7], [&] {
+  static std::once_flag attr_once[64];  // function attributes are per device
+  std::call_once(attr_once[ctx->device & 63], [&] {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   });
   // persistent grid: one CTA (CG=1) or CTA pair (CG=2) per tile slot, <= #SMs
