@@ -199,3 +199,48 @@ def test_stack_equals_layers(fm):
         cur = s.backward(cur).clone()
     assert torch.equal(cur, dx)
     assert torch.equal(singles[-1].grads.d_w1, g_last)
+
+
+def test_stack_expert_parallel_equals_single_worker(fm):
+    """cfg4's stack under expert parallelism (scaled down, W=2 ranks as threads
+    on this GPU, one shared context + peer-memory exchange per rank): equals
+    the single-worker stack on the concatenated batch bit for bit."""
+    import threading
+
+    from paper_2103_13262_b200.workloads import MoEStack
+
+    W, n, d, h, el, k, L = 2, 512, 128, 256, 4, 2, 3
+    g = torch.Generator().manual_seed(4)
+    xs = [(torch.rand(n, d, generator=g) * 2 - 1).bfloat16() for _ in range(W)]
+    dys = [(torch.rand(n, d, generator=g) * 2 - 1).bfloat16() for _ in range(W)]
+    world = fm.World(W)
+    out, errs = [None] * W, [None] * W
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                st = MoEStack(fm.MoEConfig(n, d, h, k, el, W, 50), L, rank=r)
+                st.join(world)
+                y = st.forward(xs[r].cuda()).clone()
+                dx = st.backward(dys[r].cuda()).clone()
+                s.synchronize()
+                out[r] = (y.cpu(), dx.cpu(), st.layers[0].grads.d_w1.cpu(), st.layers[-1].ep_exchange_fused)
+        except Exception as e:  # noqa: BLE001
+            errs[r] = e
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(W)]
+    [t.start() for t in th]
+    [t.join(timeout=200) for t in th]
+    for e in errs:
+        if e is not None:
+            raise e
+    single = MoEStack(fm.MoEConfig(n * W, d, h, k, el * W, 1, 50), L)
+    y = single.forward(torch.cat(xs).cuda())
+    dx = single.backward(torch.cat(dys).cuda())
+    torch.cuda.synchronize()
+    assert all(o[3] for o in out)
+    assert torch.equal(torch.cat([o[0] for o in out]), y.cpu())
+    assert torch.equal(torch.cat([o[1] for o in out]), dx.cpu())
+    assert torch.equal(torch.cat([o[2] for o in out]), single.layers[0].grads.d_w1.cpu())
