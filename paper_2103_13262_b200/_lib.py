@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfmoe_b200.so")
+# FMOE_B200_LIB: an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("FMOE_B200_LIB") or os.path.join(HERE, "libfmoe_b200.so")
 
 F64, F32, BF16 = 0, 1, 2
 OK, ERR_SHAPE, ERR_PROTOCOL, ERR_TRANSPORT, ERR_CUDA = 0, 1, 2, 3, 4
