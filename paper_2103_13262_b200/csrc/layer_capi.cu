@@ -63,7 +63,7 @@ int fmoe_layer_routing(fmoe_layer* layer, const int32_t** topk_idx, const void**
 
 int fmoe_layer_fwd(fmoe_layer* layer, const void* x, void* y) {
   FMOE_GUARD({
-    if (!x || !y) shape_error("forward: null x or y");
+    if ((!x || !y) && L(layer)->cfg.n_b > 0) shape_error("forward: null x or y");  // empty batches may be NULL
     L(layer)->forward(x, y);
   })
 }
@@ -71,7 +71,7 @@ int fmoe_layer_fwd(fmoe_layer* layer, const void* x, void* y) {
 int fmoe_layer_fwd_routed(fmoe_layer* layer, const void* x, const int32_t* topk_idx, const void* topk_scores,
                           void* y) {
   FMOE_GUARD({
-    if (!x || !y || !topk_idx || !topk_scores) shape_error("forward_routed: null argument");
+    if ((!x || !y || !topk_idx || !topk_scores) && L(layer)->cfg.n_b > 0) shape_error("forward_routed: null argument");
     L(layer)->forward_routed(x, topk_idx, topk_scores, y);
   })
 }
@@ -84,7 +84,7 @@ int fmoe_layer_routing_grad(fmoe_layer* layer, const void** d_topk_scores) {
 
 int fmoe_layer_bwd(fmoe_layer* layer, const void* dy, void* dx) {
   FMOE_GUARD({
-    if (!dy || !dx) shape_error("backward: null dy or dx");
+    if ((!dy || !dx) && L(layer)->cfg.n_b > 0) shape_error("backward: null dy or dx");
     L(layer)->backward(dy, dx);
   })
 }

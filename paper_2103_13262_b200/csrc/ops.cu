@@ -116,6 +116,10 @@ void gate_fwd(Ctx* ctx, fmoe_dtype t, const void* x, const void* wg, int64_t n, 
 // ---------------------------------------------------------------- gate bwd
 void gate_dwg_bf16(Ctx* ctx, const void* x, const __nv_bfloat16* dz, int64_t n, int64_t d, int64_t e,
                    float* part_ws, float* d_wg) {
+  if (n == 0) {  // no tokens: the gate gradient is zero
+    if (d * e) CK(cudaMemsetAsync(d_wg, 0, (size_t)(d * e) * 4, ctx->stream));
+    return;
+  }
   const int64_t S = gate_dwg_splits(n);
   const int64_t per = ceil_div(ceil_div(n, S), 64) * 64;
   int32_t* offs = reinterpret_cast<int32_t*>(part_ws + S * d * e);
@@ -134,6 +138,7 @@ void gate_dwg_bf16(Ctx* ctx, const void* x, const __nv_bfloat16* dz, int64_t n, 
 
 void gate_dx_bf16(Ctx* ctx, const __nv_bfloat16* dz, const void* wg, int64_t n, int64_t d, int64_t e,
                   const __nv_bfloat16* d_xs, const int32_t* inverse_pos, int64_t k, void* d_x) {
+  if (n == 0) return;
   const CUtensorMap ta = tc::make_tmap(dz, e, n, e * 2, 64, 128);   // dz [n, E] K-major
   const CUtensorMap tb = tc::make_tmap(wg, e, d, e * 2, 64, 256);   // Wg^T: B(k=e, n=c) = Wg[c][e], K-major
   tc::Params p{};
