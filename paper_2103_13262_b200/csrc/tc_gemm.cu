@@ -23,7 +23,11 @@ struct Cfg {
   // chunk is stored as two halves).  One tile per warp keeps 6 pipeline
   // stages in shared memory.
   static constexpr bool TMA_STORE = EPI == EPI_BF16 || EPI == EPI_MASK_BF16 || EPI == EPI_F32;
-  static constexpr int OUT_ROW_BYTES = 64;
+#ifndef FMOE_TC_F32_ROW_BYTES
+#define FMOE_TC_F32_ROW_BYTES 64  // fp32 staging rows: 64 B (16 columns, two stores per chunk); 128 B
+                                  // (one 32-column store) measured 5% slower weight gradients
+#endif
+  static constexpr int OUT_ROW_BYTES = EPI == EPI_F32 ? FMOE_TC_F32_ROW_BYTES : 64;
   static constexpr int NBUF = 1;
   static constexpr int TILE_BYTES = 32 * OUT_ROW_BYTES;
   static constexpr int STORE_BYTES = TMA_STORE ? 8 * NBUF * TILE_BYTES : 0;
@@ -845,21 +849,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(buf[i & 1][j]);
             if constexpr (EPI == EPI_F32) {
               if (p.tma_out) {
-                // two 16-column halves through the warp's 32 x 64 B staging tile
-                // (64B swizzle: 16-byte chunk j of row r at r*64 + ((j ^ ((r >> 1) & 3)) << 4));
-                // rows >= M are staged as zeros and clipped by the tensor map
+                // fp32 staging (rows >= M staged as zeros, clipped by the tensor map):
+                //  64 B rows: two 16-column halves, 64B swizzle (16-byte chunk j of row r
+                //             at r*64 + ((j ^ ((r >> 1) & 3)) << 4))
+                // 128 B rows: one 32-column tile, 128B swizzle (chunk j at r*128 + ((j ^ (r & 7)) << 4))
+                constexpr int RB = C::OUT_ROW_BYTES, HALVES = 128 / RB, CPR = RB / 16;
                 const int out_row = (p.c_group_stride ? tl.g * (int)(p.c_group_stride / p.ldc) : 0) + tl.m0 +
                                     row_off + q * 32;
                 const uint32_t r = (uint32_t)lane;
                 const bool live = row < p.M;
 #pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
+                for (int hh = 0; hh < HALVES; ++hh) {
                   const uint32_t stage = smem_u32(sOut) + (uint32_t)((ew * C::NBUF + hh % C::NBUF) * C::TILE_BYTES);
                   if (lane == 0) bulk_wait_read<C::NBUF - 1>();
                   __syncwarp();
 #pragma unroll
-                  for (int j = 0; j < 4; ++j) {
-                    const uint32_t a = stage + r * 64 + (((uint32_t)j ^ ((r >> 1) & 3u)) << 4);
+                  for (int j = 0; j < CPR; ++j) {
+                    const uint32_t sw = RB == 64 ? ((r >> 1) & 3u) : (r & 7u);
+                    const uint32_t a = stage + r * RB + (((uint32_t)j ^ sw) << 4);
                     const float* src = v + hh * 16 + 4 * j;
                     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(live ? src[0] : 0.f),
                                  "f"(live ? src[1] : 0.f), "f"(live ? src[2] : 0.f), "f"(live ? src[3] : 0.f)
@@ -1000,7 +1007,7 @@ static void launch_t(Ctx* ctx, const CUtensorMap& ta, const CUtensorMap& tb, con
                       (!grouped || (p.M % (BM * CG) == 0 && p.c_group_stride == (int64_t)p.M * p.ldc));
       if (ok) {  // (TMA stores measured 1.3-1.5x faster than direct fp32 row stores)
         const int64_t rows = grouped ? (int64_t)p.M * p.n_groups : p.M;
-        tc_out = make_tmap(p.C, p.N, rows, p.ldc * 4, 16, 32, 64, true);
+        tc_out = make_tmap(p.C, p.N, rows, p.ldc * 4, C::OUT_ROW_BYTES / 4, 32, C::OUT_ROW_BYTES, true);
         q.tma_out = 1;
       }
     } else if (!p.route_out) {
