@@ -253,3 +253,21 @@ def test_allreduce_sum_rejects_bad_groups(fm):
     assert errs == [None, None]
     for r in range(2):
         assert all(isinstance(e, fm.ProtocolError) for e in res[r]), res[r]
+
+
+def test_nccl_transport_single_rank(fm):
+    """The NCCL transport initialises (one rank: NCCL refuses two ranks on one
+    GPU) and carries the operator-level collectives through it."""
+    import ctypes as C
+
+    from paper_2103_13262_b200 import _lib
+
+    ctx = fm.Context(0)
+    uid = (C.c_char * 128)()
+    _lib.check(_lib.lib.fmoe_comm_unique_id(uid, 128))
+    _lib.check(_lib.lib.fmoe_comm_init(ctx.h, uid, 128, 1, 0))
+    plan = fm.exchange_counts([3, 1, 4], ctx)
+    assert plan.world == 1 and plan.recv_counts.tolist() == [[3, 1, 4]]
+    buf = torch.arange(6, dtype=torch.float32, device="cuda").reshape(2, 3)
+    out = fm.allreduce_sum(buf.clone(), [0], ctx=ctx)
+    assert torch.equal(out.cpu(), buf.cpu())
