@@ -28,7 +28,11 @@ struct Cfg {
                                   // (one 32-column store) measured 5% slower weight gradients
 #endif
   static constexpr int OUT_ROW_BYTES = EPI == EPI_F32 ? FMOE_TC_F32_ROW_BYTES : 64;
-  static constexpr int NBUF = 1;
+#ifndef FMOE_TC_BF16_NBUF
+#define FMOE_TC_BF16_NBUF 1  // staging tiles per epilogue warp for bf16 outputs (A/B: 2 tiles cost a
+                             // pipeline stage or the 227 KB plan; both measured slower overall)
+#endif
+  static constexpr int NBUF = EPI == EPI_F32 ? 1 : FMOE_TC_BF16_NBUF;
   static constexpr int TILE_BYTES = 32 * OUT_ROW_BYTES;
   static constexpr int STORE_BYTES = TMA_STORE ? 8 * NBUF * TILE_BYTES : 0;
   // bf16 epilogues stage the bias of each warp's 128-column slice of the tile
