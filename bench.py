@@ -5,13 +5,18 @@ Workload (BASELINE.json configs[1]) at N=1: one MoE layer,
 d_model=1024, d_hidden=4096, 64 experts, top-2, 65536 tokens, bf16 storage /
 fp32 accumulation, synthetic inputs, weights from the reference's init_state
 generators.  A step = forward + backward of the layer (gate, plan, scatter,
-grouped expert GEMMs, gather-combine, and every gradient).
+grouped expert GEMMs, gather-combine, and every gradient).  At N>1 (torchrun,
+one process per GPU) the same layer runs under expert parallelism: its 64
+experts sharded 64/N per GPU, 65536 tokens per GPU -- weak scaling of the N=1
+workload, so the per-N values compare directly.  --workload cfg3|cfg4|cfg5
+runs the other BASELINE configs (cfg3: d=2048/h=8192, 8 experts and 16384
+tokens per GPU).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload ...]
 
 Timing: W warm-up steps, then exactly K steps bracketed by barrier +
 synchronize, timed with CUDA events on the layer's stream, max over ranks.
-The working set (inputs + activations + weights ~ 7 GB) is far above the
+The working set (inputs + activations + weights, several GB) is far above the
 126 MB L2, so no flush is needed between steps.  Per-stage CUDA events are
 recorded inside the same timed region (fmoe_ctx_profile) and give the
 roofline of the dominant kernel (the tcgen05 grouped GEMM).
@@ -40,10 +45,10 @@ ZIPF_S = 1.0
 
 def workload_cfg(name: str, world: int) -> dict:
     """Per-GPU shape of a BASELINE workload at `world` GPUs."""
-    if name == "cfg2":
-        if world != 1:
-            raise SystemExit("cfg2 is the single-GPU workload (use cfg3/cfg4/cfg5 at N>1)")
-        return dict(CFG2)
+    if name == "cfg2":  # the cfg2 layer (64 experts in total), 65536 tokens per GPU, sharded over the world
+        if CFG2["n_e_local"] % world:
+            raise SystemExit("cfg2 needs the world size to divide its 64 experts")
+        return dict(CFG2, n_e_local=CFG2["n_e_local"] // world)
     if name == "cfg3":
         return dict(CFG3)
     if name == "cfg4":  # 12-layer stack, 128 experts over the world, 16384 tokens/GPU
@@ -184,14 +189,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="default", choices=["default", "cfg2", "cfg3", "cfg4", "cfg5"],
-                    help="BASELINE config (SURVEY §8d); default: cfg2 at N=1, cfg3 at N>1")
+                    help="BASELINE config (SURVEY §8d); default cfg2: its layer at every N (weak scaling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0)
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if args.workload == "default":
-        args.workload = "cfg2" if world == 1 else "cfg3"
+        args.workload = "cfg2"
     cfg = workload_cfg(args.workload, world)
     if args.impl == "reference":
         return run_reference(args, world, rank, cfg)
@@ -231,8 +236,12 @@ def run_reference(args, world, rank, cfg):
 
 def workload_name(workload, cfg, world):
     if workload == "cfg2":
-        return ("cfg2: single MoE layer d_model=1024 d_hidden=4096, 64 experts top-2, 65536 tokens, "
-                "bf16 storage / fp32 accumulate, fwd+bwd")
+        if world == 1:
+            return ("cfg2: single MoE layer d_model=1024 d_hidden=4096, 64 experts top-2, 65536 tokens, "
+                    "bf16 storage / fp32 accumulate, fwd+bwd")
+        return (f"cfg2 layer under expert parallelism: d_model=1024 d_hidden=4096, 64 experts top-2 sharded "
+                f"{64 // world} per GPU over {world} GPUs, 65536 tokens per GPU (weak scaling of the N=1 "
+                "workload), bf16 storage / fp32 accumulate, fwd+bwd")
     if workload == "cfg3":
         return (f"cfg3: expert-parallel MoE layer d_model=2048 d_hidden=8192, 8 experts/GPU x {world} GPUs, "
                 "top-2, 16384 tokens/GPU, fwd+bwd")

@@ -23,7 +23,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-N, D, H, EL, K, SEED = 16384, 2048, 8192, 8, 2, 42
+N, D, H, EL, K, SEED = 16384, 2048, 8192, 8, 2, 42  # cfg3 slice per rank (--workload cfg2: the cfg2 layer)
 
 
 def time_steps(step, stream, steps, warmup):
@@ -106,7 +106,11 @@ def main():
     ap.add_argument("--world", type=int, default=2)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg2"])
     a = ap.parse_args()
+    global N, D, H, EL
+    if a.workload == "cfg2":  # 65536 tokens per rank, 64 experts in total
+        N, D, H, EL = 65536, 1024, 4096, 64 // a.world
     import paper_2103_13262_b200 as fm
 
     torch.cuda.set_device(0)
@@ -115,7 +119,7 @@ def main():
     fused = expert_parallel(fm, a.world, "peer", a.steps, a.warmup)
     trans = expert_parallel(fm, a.world, "transport", a.steps, a.warmup)
     print(json.dumps({
-        "what": f"cfg3 slices (d=2048, h=8192, {EL} experts and {N} tokens per rank, top-2) as {a.world} ranks "
+        "what": f"{a.workload} slices (d={D}, h={H}, {EL} experts and {N} tokens per rank, top-2) as {a.world} ranks "
                 "sharing one B200 vs one worker with all experts and tokens; fwd+bwd per step",
         "world": a.world, "steps": a.steps,
         "single_worker_ms": base, "single_worker_tokens_per_s": tokens / base * 1e3,
