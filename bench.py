@@ -192,6 +192,8 @@ def main():
                     help="BASELINE config (SURVEY §8d); default cfg2: its layer at every N (weak scaling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--graph", action="store_true",
+                    help="replay the single-GPU fwd+bwd step as one captured CUDA graph")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -302,8 +304,19 @@ def run_ours(args, world, rank, cfg):
         clocks = Clocks(local)  # sampled from the warm-up (under load) through the timed region
         for _ in range(max(args.warmup, 3)):
             step()
+        eager_step = step
+        if args.graph:
+            if world > 1 or wl != "cfg2":
+                raise SystemExit("--graph: the single-GPU cfg2 step only")
+            graph = torch.cuda.CUDAGraph()
+            torch.cuda.synchronize()
+            with torch.cuda.graph(graph, stream=stream):
+                step()
+            step = graph.replay
+            step()
         ctx = layer0.ctx
-        _lib.check(_lib.lib.fmoe_ctx_profile(ctx.h, args.steps * n_layers))
+        if not args.graph:  # graph replays carry no host-side stage marks; profiled eagerly below
+            _lib.check(_lib.lib.fmoe_ctx_profile(ctx.h, args.steps * n_layers))
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
@@ -321,6 +334,13 @@ def run_ours(args, world, rank, cfg):
         if dist:
             dist.barrier()
         launches = ctx.launches - launches0
+        if args.graph:  # every replay launches the captured kernels: count them from one eager step
+            l0 = ctx.launches
+            eager_step()
+            launches = (ctx.launches - l0) * args.steps
+            _lib.check(_lib.lib.fmoe_ctx_profile(ctx.h, args.steps))
+            for _ in range(args.steps):
+                eager_step()
         ms = t0.elapsed_time(t1) / args.steps
         ms_sd = statistics.stdev(per_step) if len(per_step) > 1 else 0.0
         stage = (C.c_float * len(STAGES))()
@@ -391,7 +411,8 @@ def run_ours(args, world, rank, cfg):
         "config": {"workload": workload_name(wl, cfg, world), "n_b_per_gpu": n, "d_m": d, "d_h": h,
                    "experts_per_gpu": el, "experts_total": el * world, "k": k, "layers": n_layers,
                    "parallelism": f"ep{world}" if world > 1 else "single",
-                   "l2": "working set several GB >> 126 MB L2; no flush needed"},
+                   "l2": "working set several GB >> 126 MB L2; no flush needed",
+                   "launch": "one CUDA graph per step" if args.graph else "eager stream launches"},
         "gpu_launches": launches,
         "clocks": clk,
         "roofline": {"kernel": "tc_gemm_kernel (grouped tcgen05 expert GEMM; fc1, fc2, 2x dgrad, 2x wgrad)",
@@ -401,6 +422,8 @@ def run_ours(args, world, rank, cfg):
                      "flops_per_launch": flop_gemm, "avg_launch_ms": avg_launch_ms, "traffic": traffic,
                      "peak_source": pk["src"] + " bf16 sustained (kernel timed inside a long step)"},
         "stages_ms": {k_: round(v, 4) for k_, v in stage_ms.items()},
+        "stages_source": ("eager steps after the graph-replay timed region" if args.graph
+                          else "CUDA events inside the timed region"),
         "permute_roofline": {
             "scatter_GBps": scatter_bytes / (stage_ms["scatter"] / 1e3) / 1e9 if stage_ms["scatter"] > 0 else None,
             "gather_combine_GBps": (gather_bytes / (stage_ms["gather_combine"] / 1e3) / 1e9
