@@ -1,18 +1,23 @@
 // ep.cu -- expert parallelism (moe_layer.cpp:85-91, 124-128; collectives.cpp:69-265).
 //
-// Rank r owns experts g in [r*el, (r+1)*el) (moe_layer.hpp:29-30).  Per step:
-//   forward : gate -> send plan over all E experts (reference layout: grouped by
-//             destination rank, then its local expert, then scatter order) ->
-//             scatter -> count exchange (C1) -> ONE host sync for the counts ->
-//             token exchange (C2, global_scatter) into the receive layout
-//             (local expert, source rank, source order) with 128-row aligned
-//             expert blocks -> grouped tcgen05 experts -> reverse exchange
-//             (C3, global_gather) -> gather_combine.
-//   backward: gather_combine_bwd -> C2 on d_ys -> experts backward -> C3 on
-//             d_xs -> gate backward fused with scatter_backward.
-// The plan of the forward is reused by the backward without a recount
-// (collectives.hpp:48-50).  Chunks are exchanged per (peer, local expert)
-// straight into their final slots, so the receive side needs no permute.
+// Rank r owns experts g in [r*el, (r+1)*el) (moe_layer.hpp:29-30).  The send
+// plan covers all E experts in the reference layout (grouped by destination
+// rank, then its local expert, then scatter order); the receive layout is
+// (local expert, source rank, source order) with aligned expert blocks.  The
+// forward's plan is reused by the backward without a recount
+// (collectives.hpp:48-50).  Two ways to move the rows:
+//
+//   fused (bf16, peers mapped -- peer.cuh): gate -> plan -> count all-gather
+//     into every peer (C1) -> every rank's layout on the device (no host sync)
+//     -> scatter straight into the expert ranks (C2) -> fc1 -> fc2 storing
+//     each row straight home (C3) -> gather_combine; backward: gcb writing
+//     d_ys into the expert ranks -> dgrad fc2 / fc1 storing d_xs home ->
+//     weight gradients and gate d_wg while the peers finish -> scatter_backward.
+//     Phases are ordered by epoch flags (or events inside one process).
+//   transport (f64 / f32, fallback): scatter -> count exchange (C1) -> one
+//     host sync -> grouped send/recv per (peer, local expert) chunk straight
+//     into its final slot (C2) -> experts -> reverse exchange (C3) ->
+//     gather_combine; backward on the same routes.
 #include <algorithm>
 #include <cstring>
 #include <string>
