@@ -238,6 +238,14 @@ int fmoe_layer_routing_grad(fmoe_layer* layer, const void** d_topk_scores);
  * be NULL for forward only.  Synchronises before returning. */
 int fmoe_layer_step_host(fmoe_layer* layer, const void* x_host, const void* dy_host,
                          void* y_host, void* dx_host);
+/* The same step without the final synchronisation, for loops that feed the
+ * layer from the host: step t+1's uploads run under step t's kernels and step
+ * t's downloads under step t+1's (two device buffer sets, event-ordered).
+ * The host buffers of a step must stay untouched until a later
+ * fmoe_layer_step_host_wait returns (it waits for every submitted step). */
+int fmoe_layer_step_host_async(fmoe_layer* layer, const void* x_host, const void* dy_host,
+                               void* y_host, void* dx_host);
+int fmoe_layer_step_host_wait(fmoe_layer* layer);
 
 /* train_step (moe_layer.cpp:144-205) on device: forward, mean-squared error
  * against target [n_b, d_m] (dtype) with d_y = 2*(y - target)/n, backward,

@@ -83,6 +83,7 @@ EXPORTS = [
     "fmoe_layer_fwd_routed", "fmoe_layer_routing_grad", "fmoe_layer_set_ep_exchange",
     "fmoe_layer_ep_exchange_fused", "fmoe_ep_routes", "fmoe_layer_peer_blob", "fmoe_layer_peer_connect",
     "fmoe_checkpoint_info", "fmoe_layer_load_checkpoint", "fmoe_layer_save_checkpoint",
+    "fmoe_layer_step_host_async", "fmoe_layer_step_host_wait",
 ]
 
 
@@ -150,6 +151,8 @@ def _load():
         "fmoe_a2a_rows": [vp, C.c_int, vp, i64, C.POINTER(ExchangePlanC), vp],
         "fmoe_a2a_rows_reverse": [vp, C.c_int, vp, i64, C.POINTER(ExchangePlanC), vp],
         "fmoe_layer_step_host": [vp, vp, vp, vp, vp],
+        "fmoe_layer_step_host_async": [vp, vp, vp, vp, vp],
+        "fmoe_layer_step_host_wait": [vp],
         "fmoe_comm_unique_id": [vp, i64],
         "fmoe_comm_init": [vp, vp, i64, C.c_int, C.c_int],
         "fmoe_allreduce_sum": [vp, C.c_int, vp, i64, vp, i64],

@@ -696,6 +696,18 @@ class MoELayer:
         self.ctx.use_current_stream()
         check(lib.fmoe_layer_step_host(self.h, _p(x_host), _p(dy_host), _p(y_host), _p(dx_host)))
 
+    def step_host_async(self, x_host: torch.Tensor, dy_host: Optional[torch.Tensor], y_host: torch.Tensor,
+                        dx_host: Optional[torch.Tensor] = None):
+        """Enqueue a host-buffer forward(+backward) (fmoe_layer_step_host_async):
+        the next step's uploads overlap this step's kernels.  Host buffers must
+        stay untouched until wait_host()."""
+        self.ctx.use_current_stream()
+        check(lib.fmoe_layer_step_host_async(self.h, _p(x_host), _p(dy_host), _p(y_host), _p(dx_host)))
+
+    def wait_host(self):
+        """Wait for every step_host_async submitted so far."""
+        check(lib.fmoe_layer_step_host_wait(self.h))
+
 
 def _wrap(ptr: int, shape, dtype, device, owner):
     """A torch view of library-owned device memory (kept alive by `owner`)."""

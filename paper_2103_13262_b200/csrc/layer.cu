@@ -11,6 +11,7 @@
 //   bwd: gather_combine_bwd + gate Jacobian | dgrad fc2 (relu mask, d_b1
 //        partials) | dgrad fc1 | gate dx | scatter_backward  [d_x final] |
 //        wgrad fc2 | db2 | wgrad fc1 | db1 | gate dWg (split-K) + reduce
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -116,6 +117,9 @@ Layer::Layer(Ctx* c, const fmoe_layer_config& cf) : ctx(c), cfg(cf) {
 
 Layer::~Layer() {
   ep_free(ep);
+  for (auto* evs : {hio.x_done, hio.dy_done, hio.y_ready, hio.dx_ready, hio.compute_done, hio.out_done})
+    for (int s = 0; s < 2; ++s)
+      if (evs[s]) cudaEventDestroy(evs[s]);
   for (void* p : owned) cudaFree(p);
   if (h_stage) cudaFreeHost(h_stage);
 }
@@ -268,47 +272,74 @@ void Layer::backward(const void* dy, void* dx, cudaEvent_t dx_ready) {
   ctx->prof_slot = -1;
 }
 
-// One forward+backward on host buffers.  The PCIe copies run on the context's
-// two copy streams and overlap the kernels: d_y uploads while the forward
-// runs, y downloads during the backward, and d_x (final before the weight
-// gradients, see backward) downloads while they run.  x has nothing to hide
-// behind: every stage depends on the routing of all tokens.
-void Layer::step_host(const void* x_host, const void* dy_host, void* y_host, void* dx_host) {
-  const int64_t nd = cfg.n_b * cfg.d_m;
-  const size_t bytes = (size_t)nd * es;
+// Forward+backward on host buffers.  The PCIe copies run on the context's two
+// copy streams and overlap the kernels: inside a step d_y uploads while the
+// forward runs, y downloads during the backward and d_x (final before the
+// weight gradients, see backward) while they run; across steps (the async
+// form) the next step's uploads overlap this step's kernels and this step's
+// downloads the next step's kernels, through two device buffer sets.  Set s
+// is reused by step t+2 only after step t's kernels (inputs) and downloads
+// (outputs) are done -- event-ordered, no host synchronisation.
+void Layer::host_io_setup() {
+  const size_t bytes = (size_t)(cfg.n_b * cfg.d_m) * es;
   if (!io) {
-    io = dalloc_bytes(owned, 4 * bytes);
+    io = dalloc_bytes(owned, 8 * std::max<size_t>(bytes, 16));
+    for (auto* evs : {hio.x_done, hio.dy_done, hio.y_ready, hio.dx_ready, hio.compute_done, hio.out_done})
+      for (int s = 0; s < 2; ++s) CK(cudaEventCreateWithFlags(&evs[s], cudaEventDisableTiming));
   }
   if (!ctx->copy_in) {
     CK(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking));
     for (auto& e : ctx->ev_io) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  cudaEvent_t ev_x = ctx->ev_io[0], ev_dy = ctx->ev_io[1], ev_y = ctx->ev_io[2], ev_dx = ctx->ev_io[3];
-  uint8_t* b = reinterpret_cast<uint8_t*>(io);
+}
+
+void Layer::step_host_submit(const void* x_host, const void* dy_host, void* y_host, void* dx_host) {
+  host_io_setup();
+  const size_t bytes = (size_t)(cfg.n_b * cfg.d_m) * es;
+  const int s = (int)(hio.seq & 1);
+  const bool reuse = hio.seq >= 2;  // set s was used by step seq-2
+  uint8_t* b = reinterpret_cast<uint8_t*>(io) + (size_t)s * 4 * bytes;
   void *x = b, *y = b + bytes, *gy = b + 2 * bytes, *gx = b + 3 * bytes;
   const bool bwd = dy_host != nullptr;
-  CK(cudaMemcpyAsync(x, x_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
-  if (bwd) {  // queued behind x on the same copy direction
-    CK(cudaEventRecord(ev_x, ctx->stream));
-    CK(cudaStreamWaitEvent(ctx->copy_in, ev_x, 0));
-    CK(cudaMemcpyAsync(gy, dy_host, bytes, cudaMemcpyHostToDevice, ctx->copy_in));
-    CK(cudaEventRecord(ev_dy, ctx->copy_in));
-  }
-  forward(x, y);
-  CK(cudaEventRecord(ev_y, ctx->stream));
-  CK(cudaStreamWaitEvent(ctx->copy_out, ev_y, 0));
-  CK(cudaMemcpyAsync(y_host, y, bytes, cudaMemcpyDeviceToHost, ctx->copy_out));
+  // uploads: after step seq-2's kernels released this set's inputs
+  if (reuse) CK(cudaStreamWaitEvent(ctx->copy_in, hio.compute_done[s], 0));
+  if (bytes) CK(cudaMemcpyAsync(x, x_host, bytes, cudaMemcpyHostToDevice, ctx->copy_in));
+  CK(cudaEventRecord(hio.x_done[s], ctx->copy_in));
   if (bwd) {
-    CK(cudaStreamWaitEvent(ctx->stream, ev_dy, 0));
-    backward(gy, gx, ev_dx);
+    if (bytes) CK(cudaMemcpyAsync(gy, dy_host, bytes, cudaMemcpyHostToDevice, ctx->copy_in));
+    CK(cudaEventRecord(hio.dy_done[s], ctx->copy_in));
+  }
+  // kernels: after the inputs landed and step seq-2's downloads left this set
+  CK(cudaStreamWaitEvent(ctx->stream, hio.x_done[s], 0));
+  if (reuse) CK(cudaStreamWaitEvent(ctx->stream, hio.out_done[s], 0));
+  forward(x, y);
+  CK(cudaEventRecord(hio.y_ready[s], ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->copy_out, hio.y_ready[s], 0));
+  if (y_host && bytes) CK(cudaMemcpyAsync(y_host, y, bytes, cudaMemcpyDeviceToHost, ctx->copy_out));
+  if (bwd) {
+    CK(cudaStreamWaitEvent(ctx->stream, hio.dy_done[s], 0));
+    backward(gy, gx, hio.dx_ready[s]);
     if (dx_host) {
-      CK(cudaStreamWaitEvent(ctx->copy_out, ev_dx, 0));
-      CK(cudaMemcpyAsync(dx_host, gx, bytes, cudaMemcpyDeviceToHost, ctx->copy_out));
+      CK(cudaStreamWaitEvent(ctx->copy_out, hio.dx_ready[s], 0));
+      if (bytes) CK(cudaMemcpyAsync(dx_host, gx, bytes, cudaMemcpyDeviceToHost, ctx->copy_out));
     }
   }
-  CK(cudaStreamSynchronize(ctx->copy_out));
-  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaEventRecord(hio.compute_done[s], ctx->stream));
+  CK(cudaEventRecord(hio.out_done[s], ctx->copy_out));
+  ++hio.seq;
+}
+
+void Layer::step_host_wait() {
+  if (hio.seq == 0) return;
+  const int s = (int)((hio.seq - 1) & 1);  // the last step: its streams are ordered after the earlier ones
+  CK(cudaEventSynchronize(hio.out_done[s]));
+  CK(cudaEventSynchronize(hio.compute_done[s]));
+}
+
+void Layer::step_host(const void* x_host, const void* dy_host, void* y_host, void* dx_host) {
+  step_host_submit(x_host, dy_host, y_host, dx_host);
+  step_host_wait();
 }
 
 }  // namespace fmoe_b200

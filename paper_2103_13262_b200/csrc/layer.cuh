@@ -33,8 +33,13 @@ struct Layer {
   float* part = nullptr;   // gate d_wg split-K partials
   float* tpart = nullptr;  // expert bias-gradient tile partials
   uint32_t* relu_bits = nullptr;  // bf16: hidden > 0 bitmap (fc1 -> dgrad fc2)
-  // host-buffer step
+  // host-buffer steps: two device buffer sets (x, y, dy, dx each) and their events
   void* io = nullptr;
+  struct HostIO {
+    cudaEvent_t x_done[2] = {}, dy_done[2] = {}, y_ready[2] = {}, dx_ready[2] = {}, compute_done[2] = {},
+                out_done[2] = {};
+    int64_t seq = 0;
+  } hio;
   void* h_stage = nullptr;
   // training step (train.cu): output, d_y, d_x, loss scratch; fp32 masters of
   // the bf16 weights (widened on the first step after init / an explicit resync)
@@ -58,6 +63,9 @@ struct Layer {
   double train_step(const void* x, const void* target, double lr);
   void sgd(void* param, float* master, const void* grad, int64_t n, double lr, bool weight);
   void step_host(const void* x_host, const void* dy_host, void* y_host, void* dx_host);
+  void step_host_submit(const void* x_host, const void* dy_host, void* y_host, void* dx_host);
+  void step_host_wait();
+  void host_io_setup();
   void load_checkpoint(const char* path);  // checkpoint.cu
   void save_checkpoint(const char* path);
   void ep_alloc();

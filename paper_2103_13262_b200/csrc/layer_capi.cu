@@ -107,4 +107,14 @@ int fmoe_layer_step_host(fmoe_layer* layer, const void* x_host, const void* dy_h
   })
 }
 
+int fmoe_layer_step_host_async(fmoe_layer* layer, const void* x_host, const void* dy_host, void* y_host,
+                               void* dx_host) {
+  FMOE_GUARD({
+    if ((!x_host || !y_host) && L(layer)->cfg.n_b > 0) shape_error("step_host_async: null x or y");
+    L(layer)->step_host_submit(x_host, dy_host, y_host, dx_host);
+  })
+}
+
+int fmoe_layer_step_host_wait(fmoe_layer* layer) { FMOE_GUARD(L(layer)->step_host_wait()) }
+
 }  // extern "C"

@@ -379,6 +379,25 @@ def test_layer_step_host(fm):
     assert torch.equal(y, y2.cpu()) and torch.equal(dx, dx2.cpu())
 
 
+def test_layer_step_host_async_pipeline(fm):
+    """Back-to-back async host steps (uploads of step t+1 under the kernels of
+    step t, two device buffer sets) give every step's eager results."""
+    n, d, h, e, k = 1024, 128, 256, 16, 2
+    layer = fm.MoELayer(fm.MoEConfig(n, d, h, k, e, 1, 9), dtype=torch.bfloat16)
+    steps = 5
+    xs = [torch.randn(n, d).bfloat16().pin_memory() for _ in range(steps)]
+    dys = [torch.randn(n, d).bfloat16().pin_memory() for _ in range(steps)]
+    ys = [torch.empty(n, d, dtype=torch.bfloat16).pin_memory() for _ in range(steps)]
+    dxs = [torch.empty(n, d, dtype=torch.bfloat16).pin_memory() for _ in range(steps)]
+    for i in range(steps):
+        layer.step_host_async(xs[i], dys[i], ys[i], dxs[i])
+    layer.wait_host()
+    for i in range(steps):
+        y = layer.forward(xs[i].cuda())
+        dx = layer.backward(dys[i].cuda())
+        assert torch.equal(ys[i], y.cpu()) and torch.equal(dxs[i], dx.cpu()), i
+
+
 def test_layer_shape_errors(fm):
     with pytest.raises(fm.ShapeError):
         fm.MoELayer(fm.MoEConfig(8, 64, 64, 3, 2, 1, 0), dtype=torch.float64)  # k > E
