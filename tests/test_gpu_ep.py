@@ -96,7 +96,7 @@ def check_ep_equals_single(fm, world, n, d, h, el, k, dtype, seed=3, exchange="p
 
 
 @pytest.mark.parametrize("exchange", ["peer", "transport"])
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_ep_bf16_equals_single_worker(fm, world, exchange):
     check_ep_equals_single(fm, world, n=512, d=128, h=256, el=4, k=2, dtype=torch.bfloat16, exchange=exchange)
 
@@ -271,3 +271,53 @@ def test_nccl_transport_single_rank(fm):
     buf = torch.arange(6, dtype=torch.float32, device="cuda").reshape(2, 3)
     out = fm.allreduce_sum(buf.clone(), [0], ctx=ctx)
     assert torch.equal(out.cpu(), buf.cpu())
+
+
+def test_ep_routed_equals_single_worker(fm):
+    """Injected (Zipf) routing under expert parallelism (cfg5 at N>1): the
+    fused exchange gives the single worker's results on the concatenated batch."""
+    from paper_2103_13262_b200.workloads import zipf_routing
+
+    W, n, d, h, el, k = 2, 1024, 128, 256, 8, 1
+    g = torch.Generator().manual_seed(8)
+    xs = [(torch.rand(n, d, generator=g) * 2 - 1).bfloat16() for _ in range(W)]
+    dys = [(torch.rand(n, d, generator=g) * 2 - 1).bfloat16() for _ in range(W)]
+    routes = [zipf_routing(n, el * W, k, 1.0, seed=30 + r) for r in range(W)]
+    world = fm.World(W)
+    out, errs = [None] * W, [None] * W
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                layer = fm.MoELayer(fm.MoEConfig(n, d, h, k, el, W, 9), rank=r, dtype=torch.bfloat16)
+                layer.join(world)
+                idx = torch.as_tensor(routes[r][0], device="cuda")
+                sc = torch.as_tensor(routes[r][1], device="cuda")
+                y = layer.forward_routed(xs[r].cuda(), idx, sc)
+                dx = layer.backward(dys[r].cuda())
+                s.synchronize()
+                out[r] = (y.cpu(), dx.cpu(), layer.grads.d_w2.cpu(), layer.routing_grad().cpu(),
+                          layer.ep_exchange_fused)
+                del layer
+        except Exception as e:  # noqa: BLE001
+            errs[r] = e
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(W)]
+    [t.start() for t in th]
+    [t.join(timeout=120) for t in th]
+    for e in errs:
+        if e is not None:
+            raise e
+    single = fm.MoELayer(fm.MoEConfig(n * W, d, h, k, el * W, 1, 9), dtype=torch.bfloat16)
+    idx = torch.as_tensor(np.concatenate([r[0] for r in routes]), device="cuda")
+    sc = torch.as_tensor(np.concatenate([r[1] for r in routes]), device="cuda")
+    y = single.forward_routed(torch.cat(xs).cuda(), idx, sc)
+    dx = single.backward(torch.cat(dys).cuda())
+    torch.cuda.synchronize()
+    assert all(o[4] for o in out)
+    assert torch.equal(torch.cat([o[0] for o in out]), y.cpu())
+    assert torch.equal(torch.cat([o[1] for o in out]), dx.cpu())
+    assert torch.equal(torch.cat([o[2] for o in out]), single.grads.d_w2.cpu())
+    assert torch.equal(torch.cat([o[3] for o in out]), single.routing_grad().cpu())
