@@ -5,6 +5,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "glibc_exp.cuh"
 #include "plan.cuh"
 
 namespace fmoe_b200 {
@@ -28,7 +29,12 @@ __global__ void softmax_topk_kernel(const A* __restrict__ logits, int64_t n, int
     for (int c = 0; c < e; ++c) mx = l[c] > mx ? l[c] : mx;
     A sum = A(0);
     for (int c = 0; c < e; ++c) {
-      const A v = exp(l[c] - mx);
+      // fp64 parity: glibc's exp, bit for bit (glibc_exp.cuh); fp32: CUDA expf
+      A v;
+      if constexpr (std::is_same<A, double>::value)
+        v = glibc_exp(l[c] - mx);
+      else
+        v = exp(l[c] - mx);
       s[c] = v;
       sum += v;
     }
