@@ -50,8 +50,10 @@ __device__ __forceinline__ int64_t warp_id_global() {
   return ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
 }
 
-// Pad rows of an aligned plan: warp slot `w` -> (expert, r < align).
+// Pad rows of an aligned plan: warp slot `w` -> (expert, r < align); -1 for
+// no pad row (including the grid's rounding warps past the last expert).
 __device__ __forceinline__ int64_t pad_row(const fmoe_plan& p, int64_t w) {
+  if (w >= p.n_experts * p.align) return -1;
   const int e = (int)(w / p.align), r = (int)(w % p.align);
   const int64_t row = (int64_t)p.offsets[e] + p.counts[e] + r;
   return row < p.offsets[e + 1] ? row : -1;
