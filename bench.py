@@ -194,6 +194,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--graph", action="store_true",
                     help="replay the single-GPU fwd+bwd step as one captured CUDA graph")
+    ap.add_argument("--shared-gpu", action="store_true",
+                    help="N>1 code-path check on a one-GPU box: every rank on cuda:0, gloo plumbing, peer "
+                         "buffers exchanged through it (the fused exchange over CUDA IPC); NOT a scaling number")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -258,13 +261,22 @@ def workload_name(workload, cfg, world):
 def run_ours(args, world, rank, cfg):
     import torch
 
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    shared = args.shared_gpu and world > 1
+    local = 0 if shared else int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def max_over_ranks(v: float) -> float:
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if shared else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
     import paper_2103_13262_b200 as fm
     from paper_2103_13262_b200 import _lib
     from paper_2103_13262_b200.workloads import MoEStack, zipf_routing
@@ -280,7 +292,9 @@ def run_ours(args, world, rank, cfg):
             layer0 = model.layers[0]
         else:
             model = layer0 = fm.MoELayer(mcfg, rank=rank, dtype=torch.bfloat16)
-        if world > 1:
+        if shared:
+            model.connect_peers(dist)
+        elif world > 1:
             model.connect(dist)
         g = torch.Generator(device="cuda")
         g.manual_seed(1000 + rank)
@@ -350,9 +364,7 @@ def run_ours(args, world, rank, cfg):
         # per layer-step averages
         stage_ms = {STAGES[i]: stage[i] / max(done.value, 1) for i in range(1, len(STAGES))}
         if dist:
-            t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+            ms = max_over_ranks(ms)
         tokens = n * world
         value = tokens / (ms / 1e3)
 
@@ -390,9 +402,7 @@ def run_ours(args, world, rank, cfg):
             torch.cuda.synchronize()
             sync_ms = s0.elapsed_time(s1) / 3
             if dist:
-                t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                e2e_ms = float(t.item())
+                e2e_ms = max_over_ranks(e2e_ms)
             e2e = {"value": tokens / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 2 * n * d * 2,
                    "d2h_bytes_per_step": 2 * n * d * 2,
                    "sync_call_value": tokens / (sync_ms / 1e3),
@@ -432,7 +442,9 @@ def run_ours(args, world, rank, cfg):
                    "experts_per_gpu": el, "experts_total": el * world, "k": k, "layers": n_layers,
                    "parallelism": f"ep{world}" if world > 1 else "single",
                    "l2": "working set several GB >> 126 MB L2; no flush needed",
-                   "launch": "one CUDA graph per step" if args.graph else "eager stream launches"},
+                   "launch": "one CUDA graph per step" if args.graph else "eager stream launches",
+                   **({"shared_gpu": f"all {world} ranks on ONE GPU (code-path check, gloo plumbing, fused "
+                                     "peer exchange over CUDA IPC): not a scaling number"} if shared else {})},
         "gpu_launches": launches,
         "clocks": clk,
         "roofline": {"kernel": "tc_gemm_kernel (grouped tcgen05 expert GEMM; fc1, fc2, 2x dgrad, 2x wgrad)",

@@ -32,7 +32,10 @@ struct Cfg {
 #define FMOE_TC_BF16_NBUF 1  // staging tiles per epilogue warp for bf16 outputs (A/B: 2 tiles cost a
                              // pipeline stage or the 227 KB plan; both measured slower overall)
 #endif
-  static constexpr int NBUF = EPI == EPI_F32 ? 1 : FMOE_TC_BF16_NBUF;
+#ifndef FMOE_TC_F32_NBUF
+#define FMOE_TC_F32_NBUF 1  // staging tiles per epilogue warp for fp32 (weight-gradient) outputs
+#endif
+  static constexpr int NBUF = EPI == EPI_F32 ? FMOE_TC_F32_NBUF : FMOE_TC_BF16_NBUF;
   static constexpr int TILE_BYTES = 32 * OUT_ROW_BYTES;
   static constexpr int STORE_BYTES = TMA_STORE ? 8 * NBUF * TILE_BYTES : 0;
   // bf16 epilogues stage the bias of each warp's 128-column slice of the tile
@@ -41,8 +44,11 @@ struct Cfg {
 #define FMOE_TC_SMEM_KB 200  // per-CTA shared memory the GEMM plans for: 5 stages (227 -> 6 stages
                              // measured equal in time with ~25% more DRAM traffic)
 #endif
+#ifndef FMOE_TC_F32_SMEM_KB
+#define FMOE_TC_F32_SMEM_KB FMOE_TC_SMEM_KB
+#endif
   static constexpr int BUDGET =
-      FMOE_TC_SMEM_KB * 1024 - 1280 /*align + barriers*/ - STORE_BYTES - COLSUM_BYTES - BIAS_BYTES;
+      (EPI == EPI_F32 ? FMOE_TC_F32_SMEM_KB : FMOE_TC_SMEM_KB) * 1024 - 1280 /*align + barriers*/ - STORE_BYTES - COLSUM_BYTES - BIAS_BYTES;
   static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
   static constexpr int SMEM =
       STAGES * STAGE_BYTES + STORE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + COLSUM_BYTES + BIAS_BYTES;
@@ -647,9 +653,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+#ifndef FMOE_TC_MMA_WARP
+#define FMOE_TC_MMA_WARP 1  // the whole warp runs the MMA loop, one elected lane issues
+#endif
+    if (rank == 0 && (FMOE_TC_MMA_WARP || lane == 0)) {
       // ======================= MMA issuer =========================
       constexpr uint32_t ID = idesc<BN, A_MN, B_MN, CG>();
+      // descriptors: constant fields + the 16-byte start address (bits 0..13;
+      // stage bases are 1 KiB aligned and below 228 KiB, so adding the k
+      // offsets never carries out of the field)
+      const uint64_t da0 = sdesc(smem_u32(sA), A_MN), db0 = sdesc(smem_u32(sB), B_MN);
+      constexpr uint32_t KA = A_MN ? 2048 / 16 : 32 / 16, KB = B_MN ? 2048 / 16 : 32 / 16;
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -665,19 +679,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < tl.nkb; ++kb) {
           mbar_wait(smem_u32(full + stage), phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
-          const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
+          const uint64_t ad = da0 + (uint64_t)(stage * (C::A_BYTES / 16));
+          const uint64_t bd = db0 + (uint64_t)(stage * (C::B_BYTES / 16));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = sdesc(a_addr + (A_MN ? k * 2048 : k * 32), A_MN);
-            const uint64_t bd = sdesc(b_addr + (B_MN ? k * 2048 : k * 32), B_MN);
-            if (CG == 2)
-              tc_mma_f16_pair(d_tmem, ad, bd, ID, (kb | k) != 0);
+            if (FMOE_TC_MMA_WARP)
+              tc_mma_f16_warp<CG>(d_tmem, ad + k * KA, bd + k * KB, ID, (kb | k) != 0);
+            else if (CG == 2)
+              tc_mma_f16_pair(d_tmem, ad + k * KA, bd + k * KB, ID, (kb | k) != 0);
             else
-              tc_mma_f16(d_tmem, ad, bd, ID, (kb | k) != 0);
+              tc_mma_f16(d_tmem, ad + k * KA, bd + k * KB, ID, (kb | k) != 0);
           }
-          if (CG == 2)
-            tc_commit_pair(smem_u32(empty + stage));  // frees the stage in both CTAs
+          if (FMOE_TC_MMA_WARP)
+            tc_commit_warp<CG>(smem_u32(empty + stage));  // frees the stage (in both CTAs of a pair)
+          else if (CG == 2)
+            tc_commit_pair(smem_u32(empty + stage));
           else
             tc_commit(smem_u32(empty + stage));
           if (++stage == STAGES) {
@@ -685,7 +701,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             phase ^= 1;
           }
         }
-        if (CG == 2)
+        if (FMOE_TC_MMA_WARP)
+          tc_commit_warp<CG>(smem_u32(tfull + acc));
+        else if (CG == 2)
           tc_commit_pair(smem_u32(tfull + acc));
         else
           tc_commit(smem_u32(tfull + acc));
@@ -864,7 +882,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const bool live = row < p.M;
 #pragma unroll
                 for (int hh = 0; hh < HALVES; ++hh) {
-                  const uint32_t stage = smem_u32(sOut) + (uint32_t)((ew * C::NBUF + hh % C::NBUF) * C::TILE_BYTES);
+                  const uint32_t stage = smem_u32(sOut) + (uint32_t)((ew * C::NBUF + sbuf) * C::TILE_BYTES);
                   if (lane == 0) bulk_wait_read<C::NBUF - 1>();
                   __syncwarp();
 #pragma unroll
@@ -882,6 +900,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     tma_store_2d(&tmC, stage, tl.n0 + c * 32 + hh * 16, out_row);
                     bulk_commit();
                   }
+                  sbuf = (sbuf + 1) % C::NBUF;
                 }
                 continue;
               }

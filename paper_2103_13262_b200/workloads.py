@@ -70,6 +70,12 @@ class MoEStack:
         """Expert parallelism over NCCL: one communicator for the whole stack."""
         self.ctx.init_nccl(dist, self.config.world_size, self.layers[0].rank)
 
+    def connect_peers(self, dist):
+        """Fused peer-memory exchange for every layer, buffers swapped through
+        torch.distributed (any backend); no device transport afterwards."""
+        for layer in self.layers:
+            layer.connect_peers(dist)
+
     def join(self, world: World):
         self.ctx.join_world(world, self.layers[0].rank)
 
