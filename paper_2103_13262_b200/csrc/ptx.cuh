@@ -77,6 +77,16 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, uint32_t src,
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// Store + commit by the warp's elected lane (lane 0 when the warp is converged,
+// so lane 0's bulk_wait_read / bulk_wait_all cover these groups).
+__device__ __forceinline__ void tma_store_commit_warp(const CUtensorMap* m, uint32_t src, int c0, int c1) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];\n\t"
+      "@e cp.async.bulk.commit_group;\n\t}" ::"l"(reinterpret_cast<uint64_t>(m)),
+      "r"(src), "r"(c0), "r"(c1)
+      : "memory");
+}
 // wait until at most N committed groups are still reading shared memory
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -188,6 +198,63 @@ __device__ __forceinline__ void tc_mma_f16_warp(uint32_t d_tmem, uint64_t adesc,
         "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
+}
+// Elected-lane forms of the producer's ops (the whole warp runs the loop).
+__device__ __forceinline__ void mbar_arrive_expect_tx_warp(uint32_t bar, uint32_t bytes) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(bar), "r"(bytes)
+      : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void tma_load_2d_warp(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1) {
+  if constexpr (CG == 2)
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n\t}" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n\t}" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+// One k-block (4 x K=16) and its commit under a single elect: descriptors
+// a_lo + i*KA / b_lo + i*KB, high words constant.
+template <int CG, uint32_t KA, uint32_t KB>
+__device__ __forceinline__ void tc_mma_kblock_warp(uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo,
+                                                   uint32_t b_hi, uint32_t idesc, uint32_t accumulate,
+                                                   uint32_t bar) {
+#define FMOE_KB_BODY(GRP, COMMIT)                                                          \
+  "{\n\t.reg .pred p, e;\n\t.reg .b64 a0, a1, a2, a3, b0, b1, b2, b3;\n\t"               \
+  ".reg .b32 x1, x2, x3, y1, y2, y3;\n\t"                                                 \
+  "add.u32 x1, %1, %8;\n\tadd.u32 x2, %1, %9;\n\tadd.u32 x3, %1, %10;\n\t"             \
+  "add.u32 y1, %3, %11;\n\tadd.u32 y2, %3, %12;\n\tadd.u32 y3, %3, %13;\n\t"           \
+  "mov.b64 a0, {%1, %2};\n\tmov.b64 a1, {x1, %2};\n\t"                                   \
+  "mov.b64 a2, {x2, %2};\n\tmov.b64 a3, {x3, %2};\n\t"                                   \
+  "mov.b64 b0, {%3, %4};\n\tmov.b64 b1, {y1, %4};\n\t"                                   \
+  "mov.b64 b2, {y2, %4};\n\tmov.b64 b3, {y3, %4};\n\t"                                   \
+  "setp.ne.b32 p, %6, 0;\n\t"                                                             \
+  "elect.sync _|e, 0xffffffff;\n\t"                                                       \
+  "@e tcgen05.mma.cta_group::" GRP ".kind::f16 [%0], a0, b0, %5, p;\n\t"                  \
+  "@e tcgen05.mma.cta_group::" GRP ".kind::f16 [%0], a1, b1, %5, 1;\n\t"                  \
+  "@e tcgen05.mma.cta_group::" GRP ".kind::f16 [%0], a2, b2, %5, 1;\n\t"                  \
+  "@e tcgen05.mma.cta_group::" GRP ".kind::f16 [%0], a3, b3, %5, 1;\n\t" COMMIT "}"
+  if constexpr (CG == 2)
+    asm volatile(FMOE_KB_BODY("2", "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+                                    "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster"
+                                    ".multicast::cluster.b64 [%7], m;\n\t}\n\t")
+                 ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate), "r"(bar),
+                 "n"(KA), "n"(2 * KA), "n"(3 * KA), "n"(KB), "n"(2 * KB), "n"(3 * KB)
+                 : "memory");
+  else
+    asm volatile(FMOE_KB_BODY("1", "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t")
+                 ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate), "r"(bar),
+                 "n"(KA), "n"(2 * KA), "n"(3 * KA), "n"(KB), "n"(2 * KB), "n"(3 * KB)
+                 : "memory");
+#undef FMOE_KB_BODY
 }
 template <int CG>
 __device__ __forceinline__ void tc_commit_warp(uint32_t bar) {

@@ -536,10 +536,7 @@ __device__ __forceinline__ void drain_bf16(const Params& p, const Tile& tl, cons
     }
     fence_proxy_async_smem();
     __syncwarp();
-    if (lane == 0) {
-      tma_store_2d(tmC, stage, tl.n0 + c * 32, out_row);
-      bulk_commit();
-    }
+    tma_store_commit_warp(tmC, stage, tl.n0 + c * 32, out_row);
     sbuf = (sbuf + 1) % NBUF;
     if constexpr (COLSUM) colsum_smem[q * BN + c * 32 + lane] = warp_transpose_sum(v, lane);
   }
@@ -610,7 +607,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int n_off = (int)rank * (BN / CG);        // this CTA's B rows (N) inside the tile
 
   if (warp == 0) {
-    if (lane == 0) {
+#ifndef FMOE_TC_TMA_WARP
+#define FMOE_TC_TMA_WARP 1  // the whole warp runs the producer loop, one elected lane issues
+#endif
+    if (FMOE_TC_TMA_WARP || lane == 0) {
       // ======================= TMA producer =======================
       int stage = 0;
       uint32_t phase = 0;
@@ -622,11 +622,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < tl.nkb; ++kb) {
           mbar_wait(smem_u32(empty + stage), phase ^ 1);
           const uint32_t fb = smem_u32(full + stage);
-          if (rank == 0) mbar_arrive_expect_tx(fb, CG * C::STAGE_BYTES);
+          if (rank == 0) {
+            if (FMOE_TC_TMA_WARP)
+              mbar_arrive_expect_tx_warp(fb, CG * C::STAGE_BYTES);
+            else
+              mbar_arrive_expect_tx(fb, CG * C::STAGE_BYTES);
+          }
           const uint32_t a_dst = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_dst = smem_u32(sB + stage * C::B_BYTES);
           auto load = [&](uint32_t dst, const CUtensorMap* m, int c0, int c1) {
-            if (CG == 2)
+            if (FMOE_TC_TMA_WARP)
+              tma_load_2d_warp<CG>(dst, m, fb, c0, c1);
+            else if (CG == 2)
               tma_load_2d_pair(dst, m, fb, c0, c1);
             else
               tma_load_2d(dst, m, fb, c0, c1);
@@ -654,7 +661,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 1) {
 #ifndef FMOE_TC_MMA_WARP
-#define FMOE_TC_MMA_WARP 1  // the whole warp runs the MMA loop, one elected lane issues
+#define FMOE_TC_MMA_WARP 3  // 3: whole warp, one elected lane issues each k-block (4 MMAs + commit) in one asm; 1: per MMA; 0: lane 0 only
 #endif
     if (rank == 0 && (FMOE_TC_MMA_WARP || lane == 0)) {
       // ======================= MMA issuer =========================
@@ -681,21 +688,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tc_fence_after();
           const uint64_t ad = da0 + (uint64_t)(stage * (C::A_BYTES / 16));
           const uint64_t bd = db0 + (uint64_t)(stage * (C::B_BYTES / 16));
+          if constexpr (FMOE_TC_MMA_WARP == 3) {
+            static_assert(BK / 16 == 4, "k-block issue form assumes BK = 64");
+            // 4 x K=16 and the commit that frees the stage (in both CTAs of a pair)
+            tc_mma_kblock_warp<CG, KA, KB>(d_tmem, (uint32_t)ad, (uint32_t)(da0 >> 32), (uint32_t)bd,
+                                           (uint32_t)(db0 >> 32), ID, kb != 0, smem_u32(empty + stage));
+          } else {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
+            for (int k = 0; k < BK / 16; ++k) {
+              if (FMOE_TC_MMA_WARP)
+                tc_mma_f16_warp<CG>(d_tmem, ad + k * KA, bd + k * KB, ID, (kb | k) != 0);
+              else if (CG == 2)
+                tc_mma_f16_pair(d_tmem, ad + k * KA, bd + k * KB, ID, (kb | k) != 0);
+              else
+                tc_mma_f16(d_tmem, ad + k * KA, bd + k * KB, ID, (kb | k) != 0);
+            }
             if (FMOE_TC_MMA_WARP)
-              tc_mma_f16_warp<CG>(d_tmem, ad + k * KA, bd + k * KB, ID, (kb | k) != 0);
+              tc_commit_warp<CG>(smem_u32(empty + stage));
             else if (CG == 2)
-              tc_mma_f16_pair(d_tmem, ad + k * KA, bd + k * KB, ID, (kb | k) != 0);
+              tc_commit_pair(smem_u32(empty + stage));
             else
-              tc_mma_f16(d_tmem, ad + k * KA, bd + k * KB, ID, (kb | k) != 0);
+              tc_commit(smem_u32(empty + stage));
           }
-          if (FMOE_TC_MMA_WARP)
-            tc_commit_warp<CG>(smem_u32(empty + stage));  // frees the stage (in both CTAs of a pair)
-          else if (CG == 2)
-            tc_commit_pair(smem_u32(empty + stage));
-          else
-            tc_commit(smem_u32(empty + stage));
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -896,10 +910,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                   }
                   fence_proxy_async_smem();
                   __syncwarp();
-                  if (lane == 0) {
-                    tma_store_2d(&tmC, stage, tl.n0 + c * 32 + hh * 16, out_row);
-                    bulk_commit();
-                  }
+                  tma_store_commit_warp(&tmC, stage, tl.n0 + c * 32 + hh * 16, out_row);
                   sbuf = (sbuf + 1) % C::NBUF;
                 }
                 continue;
@@ -915,13 +926,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (C::TMA_STORE && p.tma_out) {
               fence_proxy_async_smem();
               __syncwarp();
-              if (lane == 0) {
-                // output row: group base (weight-gradient groups) + tile row + warp slab
-                const int out_row = (p.c_group_stride ? tl.g * (int)(p.c_group_stride / p.ldc) : 0) + tl.m0 +
-                                    row_off + q * 32;
-                tma_store_2d(&tmC, stage, tl.n0 + c * 32, out_row);
-                bulk_commit();
-              }
+              // output row: group base (weight-gradient groups) + tile row + warp slab
+              const int out_row = (p.c_group_stride ? tl.g * (int)(p.c_group_stride / p.ldc) : 0) + tl.m0 +
+                                  row_off + q * 32;
+              tma_store_commit_warp(&tmC, stage, tl.n0 + c * 32, out_row);
               sbuf = (sbuf + 1) % C::NBUF;
             }
             if (p.colsum_part) {  // column sums of the final fp32 values of this tile
