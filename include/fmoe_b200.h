@@ -221,6 +221,9 @@ int fmoe_layer_routing(fmoe_layer* layer, const int32_t** topk_idx, const void**
 int fmoe_layer_fwd(fmoe_layer* layer, const void* x, void* y);
 /* backward (moe_layer.cpp:112-142): dy -> dx and parameter gradients. */
 int fmoe_layer_bwd(fmoe_layer* layer, const void* dy, void* dx);
+/* Aliases of fmoe_layer_fwd / fmoe_layer_bwd under the fmoe_moe_* names. */
+int fmoe_moe_fwd(fmoe_layer* layer, const void* x, void* y);
+int fmoe_moe_bwd(fmoe_layer* layer, const void* dy, void* dx);
 /* forward with injected routing (the skewed-gate stress of SURVEY §8d cfg5:
  * a sampled IndexMatrix fed straight into build_plan, dispatch.hpp:28):
  * topk_idx [n_b, k] int32 in [0, E) (out of range -> ShapeError at
@@ -283,6 +286,10 @@ int fmoe_layer_save_checkpoint(fmoe_layer* layer, const char* path);
  * failure. */
 int fmoe_comm_unique_id(void* id_out, int64_t id_bytes);
 int fmoe_comm_init(fmoe_ctx* ctx, const void* id, int64_t id_bytes, int world, int rank);
+/* Use a communicator the caller already has (an ncclComm_t, e.g. the host
+ * framework's, one rank per GPU): world and rank are read from it, it stays
+ * owned by the caller and must outlive the context's expert-parallel calls. */
+int fmoe_comm_attach(fmoe_ctx* ctx, void* nccl_comm);
 /* In-process world (InProcWorld, transport.hpp:40-60): `world` ranks run as
  * host threads of one process, each with its own context joined to the world
  * (possibly all on one device).  Used to test the EP path on one GPU. */

@@ -75,8 +75,8 @@ EXPORTS = [
     "fmoe_plan_build", "fmoe_scatter", "fmoe_gather_combine", "fmoe_scatter_bwd",
     "fmoe_gather_combine_bwd", "fmoe_experts_fwd", "fmoe_experts_bwd", "fmoe_layer_create",
     "fmoe_layer_destroy", "fmoe_layer_init_weights", "fmoe_layer_params", "fmoe_layer_grads",
-    "fmoe_layer_routing", "fmoe_layer_fwd", "fmoe_layer_bwd", "fmoe_layer_step_host",
-    "fmoe_comm_unique_id", "fmoe_comm_init", "fmoe_world_create", "fmoe_world_destroy",
+    "fmoe_layer_routing", "fmoe_layer_fwd", "fmoe_layer_bwd", "fmoe_moe_fwd", "fmoe_moe_bwd", "fmoe_layer_step_host",
+    "fmoe_comm_unique_id", "fmoe_comm_init", "fmoe_comm_attach", "fmoe_world_create", "fmoe_world_destroy",
     "fmoe_ctx_join_world", "fmoe_exchange_counts", "fmoe_ep_layout", "fmoe_a2a_rows",
     "fmoe_a2a_rows_reverse", "fmoe_allreduce_sum", "fmoe_matmul", "fmoe_softmax_rows", "fmoe_topk_rows",
     "fmoe_experts_fwd_cached", "fmoe_experts_bwd_cached", "fmoe_layer_train_step", "fmoe_layer_sync_masters",
@@ -132,6 +132,8 @@ def _load():
         "fmoe_layer_grads": [vp, C.POINTER(vp), C.POINTER(ExpertGrads)],
         "fmoe_layer_routing": [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(Plan)],
         "fmoe_layer_fwd": [vp, vp, vp],
+        "fmoe_moe_fwd": [vp, vp, vp],
+        "fmoe_moe_bwd": [vp, vp, vp],
         "fmoe_layer_bwd": [vp, vp, vp],
         "fmoe_layer_fwd_routed": [vp, vp, vp, vp, vp],
         "fmoe_layer_routing_grad": [vp, C.POINTER(vp)],
@@ -155,6 +157,7 @@ def _load():
         "fmoe_layer_step_host_wait": [vp],
         "fmoe_comm_unique_id": [vp, i64],
         "fmoe_comm_init": [vp, vp, i64, C.c_int, C.c_int],
+        "fmoe_comm_attach": [vp, vp],
         "fmoe_allreduce_sum": [vp, C.c_int, vp, i64, vp, i64],
         "fmoe_layer_train_step": [vp, vp, vp, C.c_double, C.POINTER(C.c_double)],
         "fmoe_layer_sync_masters": [vp],

@@ -96,6 +96,11 @@ class Context:
         idb = (C.c_char * 128).from_buffer_copy(obj[0])
         check(lib.fmoe_comm_init(self.h, idb, 128, world, rank))
 
+    def attach_nccl(self, comm: int):
+        """Borrow an existing ncclComm_t (an integer handle, one rank per GPU);
+        world and rank come from the communicator, which the caller keeps."""
+        check(lib.fmoe_comm_attach(self.h, C.c_void_p(comm)))
+
 
 class World:
     """fmoe_world: `world` ranks of one process (tests, single-GPU EP runs)."""

@@ -101,8 +101,14 @@ struct NcclTransport : Transport {
     std::memcpy(&uid, id, sizeof(uid));
     NCK(ncclCommInitRank(&comm, w, uid, r));
   }
+  bool owned = true;
+  // a communicator the caller created (e.g. the host framework's): borrowed
+  explicit NcclTransport(ncclComm_t c) : comm(c), owned(false) {
+    NCK(ncclCommCount(comm, &world));
+    NCK(ncclCommUserRank(comm, &rank));
+  }
   ~NcclTransport() override {
-    if (comm) ncclCommDestroy(comm);
+    if (comm && owned) ncclCommDestroy(comm);
   }
   void group(Ctx* ctx, const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs) override {
     NCK(ncclGroupStart());
@@ -119,6 +125,8 @@ struct NcclTransport : Transport {
 Transport* make_local_transport(LocalWorld* w, int rank) { return new LocalTransport(w, rank); }
 
 Transport* make_nccl_transport(const void* id, int world, int rank) { return new NcclTransport(id, world, rank); }
+
+Transport* attach_nccl_transport(void* comm) { return new NcclTransport(reinterpret_cast<ncclComm_t>(comm)); }
 
 int nccl_unique_id(void* out, size_t bytes) {
   if (bytes < sizeof(ncclUniqueId)) shape_error("unique id buffer too small (need 128 bytes)");

@@ -60,6 +60,8 @@ struct LocalWorld {
 
 Transport* make_local_transport(LocalWorld* w, int rank);
 Transport* make_nccl_transport(const void* id, int world, int rank);
+// Borrow an existing ncclComm_t (world / rank read from it; not destroyed).
+Transport* attach_nccl_transport(void* comm);
 int nccl_unique_id(void* out, size_t bytes);
 
 }  // namespace fmoe_b200

@@ -831,6 +831,18 @@ int fmoe_comm_init(fmoe_ctx* ctx, const void* id, int64_t id_bytes, int world, i
   })
 }
 
+int fmoe_comm_attach(fmoe_ctx* ctx, void* nccl_comm) {
+  FMOE_GUARD({
+    Ctx* c = CX(ctx);
+    if (!nccl_comm) shape_error("fmoe_comm_attach: null communicator");
+    CK(cudaSetDevice(c->device));
+    Transport* t = attach_nccl_transport(nccl_comm);
+    c->world = t->world;
+    c->rank = t->rank;
+    set_transport(c, t);
+  })
+}
+
 int fmoe_world_create(int world, fmoe_world** out) {
   FMOE_GUARD({
     if (world < 1 || !out) shape_error("fmoe_world_create: bad arguments");

@@ -89,6 +89,10 @@ int fmoe_layer_bwd(fmoe_layer* layer, const void* dy, void* dx) {
   })
 }
 
+// The names SURVEY §8b lists for the C-ABI's layer entry points.
+int fmoe_moe_fwd(fmoe_layer* layer, const void* x, void* y) { return fmoe_layer_fwd(layer, x, y); }
+int fmoe_moe_bwd(fmoe_layer* layer, const void* dy, void* dx) { return fmoe_layer_bwd(layer, dy, dx); }
+
 int fmoe_layer_train_step(fmoe_layer* layer, const void* x, const void* target, double lr, double* loss) {
   FMOE_GUARD({
     if (!x || !target) shape_error("train_step: null x or target");

@@ -274,6 +274,35 @@ def test_nccl_transport_single_rank(fm):
     assert torch.equal(out.cpu(), buf.cpu())
 
 
+def test_nccl_attach_borrowed_communicator(fm):
+    """fmoe_comm_attach: a communicator the host already owns (made here
+    through libnccl itself) carries the collectives; world / rank are read from
+    it and it is still usable by its owner after the context is gone."""
+    import ctypes as C
+
+    from paper_2103_13262_b200 import _lib
+
+    nccl = C.CDLL("libnccl.so.2")  # the process's (already loaded) libnccl
+    uid = (C.c_char * 128)()
+    assert nccl.ncclGetUniqueId(uid) == 0
+    comm = C.c_void_p()
+    assert nccl.ncclCommInitRank(C.byref(comm), 1, uid, 0) == 0
+    try:
+        ctx = fm.Context(0)
+        ctx.attach_nccl(comm.value)
+        plan = fm.exchange_counts([2, 0, 5], ctx)
+        assert plan.world == 1 and plan.rank == 0 and plan.recv_counts.tolist() == [[2, 0, 5]]
+        buf = torch.arange(6, dtype=torch.float64, device="cuda").reshape(3, 2)
+        assert torch.equal(fm.allreduce_sum(buf.clone(), [0], ctx=ctx).cpu(), buf.cpu())
+        del ctx
+        n = C.c_int()
+        assert nccl.ncclCommCount(comm, C.byref(n)) == 0 and n.value == 1  # not destroyed by the context
+    finally:
+        nccl.ncclCommDestroy(comm)
+    with pytest.raises(fm.ShapeError):
+        fm.Context(0).attach_nccl(0)
+
+
 def test_ep_routed_equals_single_worker(fm):
     """Injected (Zipf) routing under expert parallelism (cfg5 at N>1): the
     fused exchange gives the single worker's results on the concatenated batch."""
