@@ -47,8 +47,11 @@ void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
 // Row alignment of bf16 expert blocks for `rows` routed rows over `experts`:
 // 256 (CTA-pair tiles, cta_group::2) once experts average >= 1024 rows, else
 // 128 -- with small experts the 256-row padding would cost more than pairs gain.
+#ifndef FMOE_PAIR_MIN_ROWS
+#define FMOE_PAIR_MIN_ROWS 1024
+#endif
 inline int64_t expert_block_align(int64_t rows, int64_t experts) {
-  return rows >= 1024 * experts ? 256 : 128;
+  return rows >= FMOE_PAIR_MIN_ROWS * experts ? 256 : 128;
 }
 // phase (bf16 only): the data-gradient GEMMs (d_pre, d_xs) and the weight
 // gradients (d_w2, d_b2, d_w1, d_b1) can be issued separately, so d_x is

@@ -282,9 +282,13 @@ def test_nccl_attach_borrowed_communicator(fm):
 
     from paper_2103_13262_b200 import _lib
 
+    class UniqueId(C.Structure):  # ncclUniqueId: 128 bytes, passed by value
+        _fields_ = [("internal", C.c_char * 128)]
+
     nccl = C.CDLL("libnccl.so.2")  # the process's (already loaded) libnccl
-    uid = (C.c_char * 128)()
-    assert nccl.ncclGetUniqueId(uid) == 0
+    nccl.ncclCommInitRank.argtypes = [C.POINTER(C.c_void_p), C.c_int, UniqueId, C.c_int]
+    uid = UniqueId()
+    assert nccl.ncclGetUniqueId(C.byref(uid)) == 0
     comm = C.c_void_p()
     assert nccl.ncclCommInitRank(C.byref(comm), 1, uid, 0) == 0
     try:
