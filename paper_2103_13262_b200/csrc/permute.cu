@@ -292,6 +292,17 @@ __global__ void gcb_kernel(const T* __restrict__ dy, const T* __restrict__ ys, i
       // the dot products as the generic loop below, so the same bits)
       constexpr int U = 4;
       const int64_t nv = d / V;
+      // gate Jacobian operands (E <= 64) fetched now, in flight with the rows
+      const int E = (int)p.n_experts;
+      const bool pre = dz != nullptr && E <= 64;
+      float s_pre[2] = {0.f, 0.f};
+      int ix_pre[2] = {0, 0};
+      if (pre) {
+        const float* s = scores + i * E;
+        if (lane < E) s_pre[0] = __ldg(s + lane);
+        if (lane + 32 < E) s_pre[1] = __ldg(s + lane + 32);
+        for (int j = 0; j < k; ++j) ix_pre[j] = __ldg(topk_idx + i * k + j);
+      }
       T* dr[2];
       const T* yr[2];
       A wt[2], part[2];
@@ -350,6 +361,24 @@ __global__ void gcb_kernel(const T* __restrict__ dy, const T* __restrict__ ys, i
         for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
         if (lane == 0) d_w[i * k + j] = (S)dot;
         dw_f[j] = (float)dot;
+      }
+      if (pre) {  // the general tail below, from registers (same operations, same bits)
+        float dot = 0.f;
+        for (int j = 0; j < k; ++j) {
+          const int ix = ix_pre[j];
+          const float sx = __shfl_sync(0xffffffffu, (ix >> 5) ? s_pre[1] : s_pre[0], ix & 31);
+          dot = fmaf(dw_f[j], sx, dot);
+        }
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int e = lane + 32 * h2;
+          if (e >= E) break;
+          float dse = 0.f;
+          for (int j = 0; j < k; ++j)
+            if (ix_pre[j] == e) dse += dw_f[j];
+          dz[i * E + e] = __float2bfloat16_rn(s_pre[h2] * (dse - dot));
+        }
+        return;
       }
       goto gate_jacobian;
     }
