@@ -81,8 +81,17 @@ __global__ void plan_scan(int32_t* __restrict__ chunk_hist, int n_chunks, int n_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   // phase 1: per-expert totals (one warp per expert column, lanes over chunks)
   for (int e = warp; e < n_experts; e += nwarps) {
-    int s = 0;
-    for (int c = lane; c < n_chunks; c += 32) s += chunk_hist[(int64_t)e * n_chunks + c];
+    // 8 loads in flight per lane (the summation order is irrelevant: integers)
+    const int32_t* col = chunk_hist + (int64_t)e * n_chunks;
+    int s = 0, c = lane;
+    for (; c + 7 * 32 < n_chunks; c += 8 * 32) {
+      int v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = col[c + u * 32];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; c < n_chunks; c += 32) s += col[c];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) {
@@ -124,14 +133,30 @@ __global__ void plan_scan(int32_t* __restrict__ chunk_hist, int n_chunks, int n_
     const int cper = (n_chunks + 31) / 32;
     const int c0 = lane * cper, c1 = min(c0 + cper, n_chunks);
     int32_t* col = chunk_hist + (int64_t)e * n_chunks;
-    int loc = 0;
-    for (int c = c0; c < c1; ++c) loc += col[c];
-    const int ex = warp_incl_scan(loc, lane) - loc;
-    int b = off + ex;
-    for (int c = c0; c < c1; ++c) {
-      const int h = col[c];
-      col[c] = b;
-      b += h;
+    constexpr int kReg = 16;  // a lane's run of chunk counts held in registers (n_chunks <= 512)
+    if (cper <= kReg) {
+      int v[kReg];
+#pragma unroll
+      for (int u = 0; u < kReg; ++u) v[u] = c0 + u < c1 ? col[c0 + u] : 0;
+      int loc = 0;
+#pragma unroll
+      for (int u = 0; u < kReg; ++u) loc += v[u];
+      int b = off + warp_incl_scan(loc, lane) - loc;
+#pragma unroll
+      for (int u = 0; u < kReg; ++u) {
+        if (c0 + u < c1) col[c0 + u] = b;
+        b += v[u];
+      }
+    } else {
+      int loc = 0;
+      for (int c = c0; c < c1; ++c) loc += col[c];
+      const int ex = warp_incl_scan(loc, lane) - loc;
+      int b = off + ex;
+      for (int c = c0; c < c1; ++c) {
+        const int h = col[c];
+        col[c] = b;
+        b += h;
+      }
     }
     const int cnt = counts[e];
     const int end = off + (cnt + align - 1) / align * align;
