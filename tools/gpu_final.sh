@@ -10,6 +10,6 @@ echo "smoke exit $?" >> gpurun_out/smoke.log
 bash tools/gpu_profile.sh
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-for w in cfg5 cfg4; do
+for w in cfg5 cfg4 cfg3; do
 timeout 900 python bench.py --workload $w --steps 10 > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err
 done
