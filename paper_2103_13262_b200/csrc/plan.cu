@@ -6,14 +6,14 @@
 //                    __match_any_sync-aggregated shared-memory histogram
 //                    -> chunk_hist[e][c] (expert-major); out-of-range index
 //                    -> error flag.
-//   K2b plan_scan  : one CTA.  counts[e] = sum_c chunk_hist[e][c]; aligned
-//                    exclusive scan -> offsets; per-chunk bases (in place)
-//                    base[e][c] = offsets[e] + sum_{c'<c} hist[e][c'];
+//   K2b plan_colscan: one warp per expert, all in parallel: counts[e] and,
+//                    in place, rel[e][c] = sum_{c'<c} hist[e][c'].
+//   K2c plan_offsets: one CTA: aligned exclusive scan of counts -> offsets;
 //                    padding rows (src_row = -1); 128-row tile -> expert table.
-//   K2c plan_rank  : re-walks each chunk in order; within a 32-wide step the
+//   K2d plan_rank  : re-walks each chunk in order; within a 32-wide step the
 //                    rank of a lane among equal experts is popc(match & lt),
 //                    across steps a per-warp shared counter carries it.  Hence
-//                    pos(f) = base[c][e] + #{f' < f in chunk c : idx[f'] = e},
+//                    pos(f) = offsets[e] + rel[e][c] + #{f' < f in chunk c : idx[f'] = e},
 //                    exactly the reference's row-major fill order.
 // Integer-exact by construction; checked bit-for-bit against the oracle.
 #include <mutex>
@@ -26,7 +26,7 @@ namespace fmoe_b200 {
 constexpr int kChunk = 512;       // selections per warp chunk
 constexpr int kWarpsPerCta = 4;
 
-// chunk_hist is expert-major ([E][n_chunks]) so plan_scan reads each
+// chunk_hist is expert-major ([E][n_chunks]) so plan_colscan reads each
 // expert's column contiguously.
 __global__ void plan_hist(const int32_t* __restrict__ idx, int64_t nk, int n_experts, int n_chunks,
                           int32_t* __restrict__ chunk_hist, int* __restrict__ err) {
@@ -70,42 +70,55 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
   return v;
 }
 
-// One CTA of 1024 threads.
-__global__ void plan_scan(int32_t* __restrict__ chunk_hist, int n_chunks, int n_experts, int align,
-                          int64_t capacity, int32_t* __restrict__ counts, int32_t* __restrict__ offsets,
-                          int32_t* __restrict__ src_row, int32_t* __restrict__ tile_expert,
-                          int32_t* __restrict__ n_tiles) {
-  extern __shared__ int32_t sh[];  // [n_experts] aligned counts, then scan scratch
+// K2b: one warp per expert, all experts in parallel: counts[e] and, in
+// place, each chunk's exclusive prefix inside its expert column (chunk order).
+__global__ void plan_colscan(int32_t* __restrict__ chunk_hist, int n_chunks, int n_experts,
+                             int32_t* __restrict__ counts) {
+  const int e = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (e >= n_experts) return;
+  int32_t* col = chunk_hist + (int64_t)e * n_chunks;
+  constexpr int R = 8;  // consecutive chunks per lane per pass
+  int carry = 0;
+  for (int c0 = 0; c0 < n_chunks; c0 += 32 * R) {
+    const int base = c0 + lane * R;
+    int v[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) v[u] = base + u < n_chunks ? col[base + u] : 0;
+    int loc = 0;
+#pragma unroll
+    for (int u = 0; u < R; ++u) loc += v[u];
+    const int incl = warp_incl_scan(loc, lane);
+    int b = carry + incl - loc;
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      if (base + u < n_chunks) col[base + u] = b;
+      b += v[u];
+    }
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (lane == 0) counts[e] = carry;
+}
+
+// K2c: one CTA: aligned exclusive scan of the counts -> offsets; padding rows
+// (src_row = -1); 128-row tile -> expert table.
+__global__ void plan_offsets(const int32_t* __restrict__ counts, int n_experts, int align,
+                             int32_t* __restrict__ offsets, int32_t* __restrict__ src_row,
+                             int32_t* __restrict__ tile_expert, int32_t* __restrict__ n_tiles) {
+  extern __shared__ int32_t sh[];  // [n_experts] aligned counts -> exclusive offsets
   int32_t* acnt = sh;
   __shared__ int32_t warp_tot[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  // phase 1: per-expert totals (one warp per expert column, lanes over chunks)
-  for (int e = warp; e < n_experts; e += nwarps) {
-    // 8 loads in flight per lane (the summation order is irrelevant: integers)
-    const int32_t* col = chunk_hist + (int64_t)e * n_chunks;
-    int s = 0, c = lane;
-    for (; c + 7 * 32 < n_chunks; c += 8 * 32) {
-      int v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = col[c + u * 32];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) s += v[u];
-    }
-    for (; c < n_chunks; c += 32) s += col[c];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) {
-      counts[e] = s;
-      acnt[e] = (s + align - 1) / align * align;
-    }
+  for (int e = threadIdx.x; e < n_experts; e += blockDim.x) {
+    const int c = counts[e];
+    acnt[e] = (c + align - 1) / align * align;
   }
   __syncthreads();
-  // phase 2: exclusive scan of aligned counts (thread t owns a contiguous run)
   const int per = (n_experts + blockDim.x - 1) / blockDim.x;
   const int lo = threadIdx.x * per, hi = min(lo + per, n_experts);
   int run = 0;
   for (int e = lo; e < hi; ++e) run += acnt[e];
-  int incl = warp_incl_scan(run, lane);
+  const int incl = warp_incl_scan(run, lane);
   if (lane == 31) warp_tot[warp] = incl;
   __syncthreads();
   if (warp == 0) {
@@ -117,7 +130,7 @@ __global__ void plan_scan(int32_t* __restrict__ chunk_hist, int n_chunks, int n_
   int base = incl - run + (warp > 0 ? warp_tot[warp - 1] : 0);
   for (int e = lo; e < hi; ++e) {
     const int a = acnt[e];
-    acnt[e] = base;  // now: exclusive offset
+    acnt[e] = base;
     offsets[e] = base;
     base += a;
   }
@@ -126,49 +139,18 @@ __global__ void plan_scan(int32_t* __restrict__ chunk_hist, int n_chunks, int n_
     if (n_tiles) n_tiles[0] = base / 128;
   }
   __syncthreads();
-  // phase 3: chunk bases, padding rows, tile table
   for (int e = warp; e < n_experts; e += nwarps) {
-    const int off = acnt[e];
-    // lanes own contiguous chunk ranges so the scan follows chunk order
-    const int cper = (n_chunks + 31) / 32;
-    const int c0 = lane * cper, c1 = min(c0 + cper, n_chunks);
-    int32_t* col = chunk_hist + (int64_t)e * n_chunks;
-    constexpr int kReg = 16;  // a lane's run of chunk counts held in registers (n_chunks <= 512)
-    if (cper <= kReg) {
-      int v[kReg];
-#pragma unroll
-      for (int u = 0; u < kReg; ++u) v[u] = c0 + u < c1 ? col[c0 + u] : 0;
-      int loc = 0;
-#pragma unroll
-      for (int u = 0; u < kReg; ++u) loc += v[u];
-      int b = off + warp_incl_scan(loc, lane) - loc;
-#pragma unroll
-      for (int u = 0; u < kReg; ++u) {
-        if (c0 + u < c1) col[c0 + u] = b;
-        b += v[u];
-      }
-    } else {
-      int loc = 0;
-      for (int c = c0; c < c1; ++c) loc += col[c];
-      const int ex = warp_incl_scan(loc, lane) - loc;
-      int b = off + ex;
-      for (int c = c0; c < c1; ++c) {
-        const int h = col[c];
-        col[c] = b;
-        b += h;
-      }
-    }
-    const int cnt = counts[e];
+    const int off = acnt[e], cnt = counts[e];
     const int end = off + (cnt + align - 1) / align * align;
     for (int r = off + cnt + lane; r < end; r += 32) src_row[r] = -1;
     if (tile_expert)
       for (int t = off / 128 + lane; t < end / 128; t += 32) tile_expert[t] = e;
   }
-  (void)capacity;
 }
 
 __global__ void plan_rank(const int32_t* __restrict__ idx, int64_t nk, int k, int n_experts, int n_chunks,
-                          const int32_t* __restrict__ chunk_base, int32_t* __restrict__ src_row,
+                          const int32_t* __restrict__ chunk_base, const int32_t* __restrict__ offsets,
+                          int32_t* __restrict__ src_row,
                           int32_t* __restrict__ slot, int32_t* __restrict__ inverse_pos) {
   extern __shared__ int32_t sh[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -190,7 +172,7 @@ __global__ void plan_rank(const int32_t* __restrict__ idx, int64_t nk, int k, in
 #pragma unroll
   for (int t = 0; t < kChunk / 32; ++t) {
     if (keys[t] >= n_experts || keys[t] < 0) keys[t] = -1;
-    bases[t] = keys[t] >= 0 ? __ldg(base + (int64_t)keys[t] * n_chunks) : 0;
+    bases[t] = keys[t] >= 0 ? __ldg(base + (int64_t)keys[t] * n_chunks) + __ldg(offsets + keys[t]) : 0;
   }
 #pragma unroll
   for (int t = 0; t < kChunk / 32; ++t) {
@@ -239,7 +221,7 @@ void plan_build(Ctx* ctx, const int32_t* topk_idx, const fmoe_plan& p) {
   std::call_once(attr_once[ctx->device & 63], [] {
     CK(cudaFuncSetAttribute(plan_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CK(cudaFuncSetAttribute(plan_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaFuncSetAttribute(plan_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(plan_offsets, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   });
   const unsigned grid = (unsigned)std::max<int64_t>(1, ceil_div(chunks, kWarpsPerCta));
   if (nk > 0) {
@@ -247,14 +229,19 @@ void plan_build(Ctx* ctx, const int32_t* topk_idx, const fmoe_plan& p) {
                                                               ctx->d_error);
     CK_LAUNCH(ctx);
   }
-  plan_scan<<<1, 1024, (size_t)E * 4, ctx->stream>>>(chunk_hist, (int)chunks, E, (int)p.align,
-                                                     p.capacity, p.counts, p.offsets, p.src_row,
-                                                     p.align % 128 == 0 ? p.tile_expert : nullptr,
-                                                     p.n_tiles);
+  if (nk > 0) {
+    plan_colscan<<<(unsigned)ceil_div((int64_t)E * 32, 256), 256, 0, ctx->stream>>>(chunk_hist, (int)chunks, E,
+                                                                                    p.counts);
+    CK_LAUNCH(ctx);
+  } else {
+    CK(cudaMemsetAsync(p.counts, 0, (size_t)E * 4, ctx->stream));
+  }
+  plan_offsets<<<1, 1024, (size_t)E * 4, ctx->stream>>>(p.counts, E, (int)p.align, p.offsets, p.src_row,
+                                                        p.align % 128 == 0 ? p.tile_expert : nullptr, p.n_tiles);
   CK_LAUNCH(ctx);
   if (nk > 0) {
     plan_rank<<<grid, 32 * kWarpsPerCta, smem, ctx->stream>>>(topk_idx, nk, (int)p.k, E, (int)chunks, chunk_hist,
-                                                              p.src_row, p.slot, p.inverse_pos);
+                                                              p.offsets, p.src_row, p.slot, p.inverse_pos);
     CK_LAUNCH(ctx);
   }
 }

@@ -21,7 +21,7 @@ OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 
 # issue order of one bf16 single-GPU step (layer.cu): data gradients first
-STEP_ORDER = ["gate", "plan_hist", "plan_scan", "plan_rank", "scatter", "fc1", "fc2", "gather_combine",
+STEP_ORDER = ["gate", "plan_hist", "plan_colscan", "plan_offsets", "plan_rank", "scatter", "fc1", "fc2", "gather_combine",
               "gcb", "dgrad_fc2", "dgrad_fc1", "gate_dx", "scatter_bwd", "wgrad_order", "wgrad_fc2", "db2_colsum",
               "db2_reduce",
               "wgrad_fc1", "db1_reduce", "gate_dwg_offsets", "gate_dwg", "gate_dwg_reduce"]
