@@ -226,8 +226,9 @@ int fmoe_moe_fwd(fmoe_layer* layer, const void* x, void* y);
 int fmoe_moe_bwd(fmoe_layer* layer, const void* dy, void* dx);
 /* forward with injected routing (the skewed-gate stress of SURVEY §8d cfg5:
  * a sampled IndexMatrix fed straight into build_plan, dispatch.hpp:28):
- * topk_idx [n_b, k] int32 in [0, E) (out of range -> ShapeError at
- * fmoe_ctx_check, as build_plan, dispatch.cpp:21-23), topk_scores [n_b, k]
+ * topk_idx [n_b, k] int32 in [0, E) (checked before any work: out of range ->
+ * ShapeError from this call, as build_plan, dispatch.cpp:21-23; the check is
+ * the one host synchronisation of the routed step), topk_scores [n_b, k]
  * in the score dtype.  The gate is skipped; the following fmoe_layer_bwd
  * yields d_x = scatter_backward(d_xs) (dispatch.cpp:80-95) with no gate term,
  * a zero gate gradient, and d(topk_scores) (gather_combine_backward's d_w,
