@@ -452,7 +452,11 @@ def run_ours(args, world, rank, cfg):
                      "frac": achieved / pk["tc_sus"], "frac_of_burst_peak": achieved / pk["tc"],
                      "frac_of_datasheet_2250": achieved / 2250.0,
                      "flops_per_launch": flop_gemm, "avg_launch_ms": avg_launch_ms, "traffic": traffic,
-                     "peak_source": pk["src"] + " bf16 sustained (kernel timed inside a long step)"},
+                     "peak_source": pk["src"] + " bf16 sustained (kernel timed inside a long step)",
+                     **({"note": ("averaged over the six expert GEMMs; with few rows per expert the weight-gradient "
+                                  "launches are bound by writing fp32 gradients (HBM), not by the tensor pipe "
+                                  "(profiles/r01h_cfg4_wgrad.md); fc1/fc2/dgrad stages in stages_ms")}
+                        if wl in ("cfg4", "cfg5") else {})},
         "stages_ms": {k_: round(v, 4) for k_, v in stage_ms.items()},
         "stages_source": ("eager steps after the graph-replay timed region" if args.graph
                           else "CUDA events inside the timed region"),
