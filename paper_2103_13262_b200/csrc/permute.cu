@@ -157,7 +157,9 @@ __global__ void gather_combine_kernel(const T* __restrict__ ys, int64_t d, fmoe_
 }
 
 // ---------------------------------------------------------- scatter_backward
-template <typename T>
+// KM: slots held in registers by the fast path (k <= KM); the k <= 2 instance
+// needs half the registers of KM = 4 (more warps per SM)
+template <typename T, int KM = 4>
 __global__ void scatter_bwd_kernel(const T* __restrict__ d_xs, int64_t d, fmoe_plan p,
                                    const T* __restrict__ addend, T* __restrict__ dx) {
   using A = AccOf<T>;
@@ -166,18 +168,18 @@ __global__ void scatter_bwd_kernel(const T* __restrict__ d_xs, int64_t d, fmoe_p
   const int lane = threadIdx.x & 31;
   if (i >= p.n_b) return;
   const int k = (int)p.k;
-  if ((d % V) == 0 && k <= 4) {
+  if ((d % V) == 0 && k <= KM) {
     // every slot's rows (and the addend) in flight together; adds in slot
     // order then the addend, as below
     constexpr int U = 4;
     const int64_t nv = d / V;
-    const T* src[4];
+    const T* src[KM];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) src[j] = j < k ? d_xs + (int64_t)__ldg(p.inverse_pos + i * k + j) * d : d_xs;
+    for (int j = 0; j < KM; ++j) src[j] = j < k ? d_xs + (int64_t)__ldg(p.inverse_pos + i * k + j) * d : d_xs;
     for (int64_t c0 = lane; c0 < nv; c0 += 32 * U) {
-      uint4 raw[4][U], ad[U];
+      uint4 raw[KM][U], ad[U];
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < KM; ++j)
 #pragma unroll
         for (int u = 0; u < U; ++u)
           if (j < k && c0 + 32 * u < nv) raw[j][u] = __ldg(reinterpret_cast<const uint4*>(src[j]) + c0 + 32 * u);
@@ -192,7 +194,7 @@ __global__ void scatter_bwd_kernel(const T* __restrict__ d_xs, int64_t d, fmoe_p
 #pragma unroll
         for (int e = 0; e < V; ++e) acc[e] = A(0);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < KM; ++j) {
           if (j >= k) break;
           A g[V];
           unpack16<T, A>(raw[j][u], g);
@@ -582,9 +584,14 @@ void scatter_bwd(Ctx* ctx, fmoe_dtype t, const void* d_xs, int64_t d, const fmoe
   const unsigned grid = (unsigned)ceil_div(p.n_b * 32, 256);
   dispatch_dtype(t, [&](auto* tag) {
     using T = std::remove_pointer_t<decltype(tag)>;
-    scatter_bwd_kernel<T><<<grid, 256, 0, ctx->stream>>>(reinterpret_cast<const T*>(d_xs), d, p,
-                                                        reinterpret_cast<const T*>(addend),
-                                                        reinterpret_cast<T*>(dx));
+    if (p.k <= 2)
+      scatter_bwd_kernel<T, 2><<<grid, 256, 0, ctx->stream>>>(reinterpret_cast<const T*>(d_xs), d, p,
+                                                             reinterpret_cast<const T*>(addend),
+                                                             reinterpret_cast<T*>(dx));
+    else
+      scatter_bwd_kernel<T, 4><<<grid, 256, 0, ctx->stream>>>(reinterpret_cast<const T*>(d_xs), d, p,
+                                                             reinterpret_cast<const T*>(addend),
+                                                             reinterpret_cast<T*>(dx));
   });
   CK_LAUNCH(ctx);
 }
