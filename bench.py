@@ -80,42 +80,89 @@ def peaks():
 
 # ------------------------------------------------------------------ clocks
 class Clocks:
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock, power and clock-event reasons sampled with NVML every
+    `period` seconds on a background thread (nvidia-smi at 100 ms gave one
+    sample in a 0.12 s timed region).  `region(True/False)` brackets the timed
+    region; the summary covers the samples taken inside it (all samples when
+    the region saw fewer than 3)."""
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, period: float = 0.005):
+        import threading
+
+        self.samples, self.in_region, self.err = [], False, None
+        self.stop_ev = threading.Event()
         try:
-            self.p = subprocess.Popen(["nvidia-smi", f"--id={device}", f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
-                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except Exception:
-            self.p = None
+            import pynvml as nv
+
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(self._nvml_index(device))
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self.bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                         "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                         "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                         "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        except Exception as e:  # no NVML: report it, never guess
+            self.nv, self.err = None, f"nvml unavailable: {e}"
+            return
+        self.period = period
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    @staticmethod
+    def _nvml_index(device: int) -> int:
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            try:
+                return int(vis.split(",")[device])
+            except (ValueError, IndexError):
+                pass
+        return device
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop_ev.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                pw = nv.nvmlDeviceGetPowerUsage(self.h) / 1e3
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((self.in_region, sm, pw, rs))
+            except Exception as e:
+                self.err = str(e)
+            time.sleep(self.period)
+
+    def region(self, inside: bool):
+        self.in_region = inside
 
     def stop(self):
-        if self.p is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.p.terminate()
-        try:
-            out = self.p.communicate(timeout=5)[0]
-        except Exception:
-            self.p.kill()
-            out = ""
-        sm, mx, reasons = [], [], set()
-        for line in out.strip().splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 6:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx.append(float(f[1]))
-            except ValueError:
-                continue
-            for name, v in zip(self.NAMES, f[2:6]):
-                if v.lower().startswith("active"):
-                    reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+        if self.nv is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err]}
+        self.stop_ev.set()
+        self.t.join(timeout=2)
+        inside = [x for x in self.samples if x[0]]
+        use = inside if len(inside) >= 3 else self.samples
+        sm = [x[1] for x in use]
+        pw = [x[2] for x in use]
+        reasons = sorted({n for x in use for n, b in self.bits.items() if x[3] & b})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "sm_mhz_min": min(sm) if sm else None, "sm_mhz_max_seen": max(sm) if sm else None,
+                "power_w_median": statistics.median(pw) if pw else None, "power_w_max": max(pw) if pw else None,
+                "samples": len(use), "samples_in_timed_region": len(inside),
+                "sampler": f"NVML every {self.period * 1e3:.0f} ms", "reasons": reasons}
+
+
+def tensor_peak(pk: dict, clk: dict):
+    """Roofline denominator for the expert GEMM: the burst cuBLAS figure when
+    the SM clock sat at its maximum through the timed region, the sustained
+    (power-capped, seconds-long) figure when it was held below it."""
+    sm, mx = clk.get("sm_mhz"), clk.get("sm_max_mhz")
+    if sm and mx and sm >= 0.97 * mx:
+        return pk["tc"], "burst (median SM clock at max through the timed region)"
+    if sm and mx:
+        return pk["tc_sus"], (f"sustained (median SM clock {sm:.0f} of {mx:.0f} MHz under the power cap; "
+                              "the burst figure needs the maximum clock)")
+    return pk["tc_sus"], "sustained (no clock samples)"
 
 
 # ------------------------------------------------------------- CPU reference
@@ -262,6 +309,9 @@ def run_ours(args, world, rank, cfg):
     import torch
 
     shared = args.shared_gpu and world > 1
+    if world > 1 and not shared:  # NCCL's INIT lines (rings, NVLS, P2P) on stderr, for the scaling runs
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     local = 0 if shared else int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
@@ -337,11 +387,13 @@ def run_ours(args, world, rank, cfg):
         launches0 = ctx.launches
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         torch.cuda.synchronize()
+        clocks.region(True)
         evs[0].record(stream)
         for i in range(args.steps):
             step()
             evs[i + 1].record(stream)
         torch.cuda.synchronize()
+        clocks.region(False)
         clk = clocks.stop()
         t0, t1 = evs[0], evs[-1]
         per_step = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
@@ -401,8 +453,60 @@ def run_ours(args, world, rank, cfg):
             s1.record(stream)
             torch.cuda.synchronize()
             sync_ms = s0.elapsed_time(s1) / 3
+            # training-loop variant (reported beside the headline, never instead of
+            # it): x arrives from pinned host memory every step (double-buffered
+            # upload on a copy stream, overlapping the previous step), d_y is
+            # device-resident as the downstream layer would leave it, d_x stays
+            # on the device for the upstream layer, and the step's result read
+            # back is one fp32 scalar (sum of y, a loss stand-in)
+            copy = torch.cuda.Stream()
+            xb = [torch.empty_like(x), torch.empty_like(x)]
+            up = [torch.cuda.Event(), torch.cuda.Event()]
+            used = [torch.cuda.Event(), torch.cuda.Event()]
+            res_d = torch.empty(e2e_steps, dtype=torch.float32, device="cuda")
+            res_h = torch.empty(e2e_steps, dtype=torch.float32).pin_memory()
+
+            def upload(i):
+                with torch.cuda.stream(copy):
+                    if i >= 2:
+                        copy.wait_event(used[i & 1])
+                    xb[i & 1].copy_(hx, non_blocking=True)
+                    up[i & 1].record(copy)
+
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0_ = torch.cuda.Event(enable_timing=True)
+            t1_ = torch.cuda.Event(enable_timing=True)
+            t0_.record(stream)
+            upload(0)
+            for i in range(e2e_steps):
+                if i + 1 < e2e_steps:
+                    upload(i + 1)
+                stream.wait_event(up[i & 1])
+                layer0.forward(xb[i & 1], y)
+                layer0.backward(dy, dx)
+                used[i & 1].record(stream)
+                torch.sum(y, dtype=torch.float32, out=res_d[i])
+                res_h[i].copy_(res_d[i], non_blocking=True)
+            t1_.record(stream)
+            torch.cuda.synchronize()
+            tl_ms = t0_.elapsed_time(t1_) / e2e_steps
             if dist:
                 e2e_ms = max_over_ranks(e2e_ms)
+                tl_ms = max_over_ranks(tl_ms)
+            # PCIe ceiling of the host-buffer path: x + dy up and y + dx down per
+            # step, full duplex, at the copy rates measured here
+            c0, c1, c2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            c0.record(stream)
+            xb[0].copy_(hx, non_blocking=True)
+            c1.record(stream)
+            hy.copy_(xb[0], non_blocking=True)
+            c2.record(stream)
+            torch.cuda.synchronize()
+            h2d_gbs = n * d * 2 / (c0.elapsed_time(c1) / 1e3) / 1e9
+            d2h_gbs = n * d * 2 / (c1.elapsed_time(c2) / 1e3) / 1e9
+            pcie_cap = tokens / max(2 * n * d * 2 / (h2d_gbs * 1e9), 2 * n * d * 2 / (d2h_gbs * 1e9))
             e2e = {"value": tokens / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 2 * n * d * 2,
                    "d2h_bytes_per_step": 2 * n * d * 2,
                    "sync_call_value": tokens / (sync_ms / 1e3),
@@ -413,9 +517,19 @@ def run_ours(args, world, rank, cfg):
                             "before it returns"),
                    "path": ("fmoe_layer_step_host_async x K + wait (pinned host x,dy -> H2D -> fwd+bwd -> "
                             "D2H y,dx every step; copy streams overlap the uploads / downloads with the "
-                            "kernels of the same and the neighbouring steps)")}
+                            "kernels of the same and the neighbouring steps)"),
+                   "pcie_ceiling_value": pcie_cap, "h2d_GBps": h2d_gbs, "d2h_GBps": d2h_gbs,
+                   "pcie_ceiling_note": ("x, dy in and y, dx out: 2 x n_b x d_m bf16 per direction per step at the "
+                                         "H2D / D2H rates measured here cap the host-buffer path at this rate "
+                                         "however fast the kernels get (DESIGN.md §6)"),
+                   "training_loop": {"value": tokens / (tl_ms / 1e3), "unit": UNIT,
+                                     "h2d_bytes_per_step": n * d * 2, "d2h_bytes_per_step": 4,
+                                     "path": ("MoELayer.forward/backward: x uploaded from pinned host memory each "
+                                              "step (copy stream, double-buffered), d_y device-resident, d_x left "
+                                              "on the device, one fp32 scalar (sum of y) read back per step")}}
 
     pk = peaks()
+    peak, peak_why = tensor_peak(pk, clk)
     # expert GEMM FLOPs of one launch (fmoe_bench.cpp:110-126): 2 * rows * d * h,
     # rows = tokens routed to this rank's experts (N*k per rank on average)
     flop_gemm = 2.0 * n * k * d * h
@@ -448,11 +562,16 @@ def run_ours(args, world, rank, cfg):
         "gpu_launches": launches,
         "clocks": clk,
         "roofline": {"kernel": "tc_gemm_kernel (grouped tcgen05 expert GEMM; fc1, fc2, 2x dgrad, 2x wgrad)",
-                     "bound": "tensor", "achieved": achieved, "peak": pk["tc_sus"], "unit": "TFLOP/s",
-                     "frac": achieved / pk["tc_sus"], "frac_of_burst_peak": achieved / pk["tc"],
+                     "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "frac_of_burst_peak": achieved / pk["tc"],
+                     "frac_of_sustained_peak": achieved / pk["tc_sus"],
+                     **({"frac_at_observed_clock": achieved / (pk["tc"] * clk["sm_mhz"] / clk["sm_max_mhz"])}
+                        if clk.get("sm_mhz") and clk.get("sm_max_mhz") else {}),
                      "frac_of_datasheet_2250": achieved / 2250.0,
                      "flops_per_launch": flop_gemm, "avg_launch_ms": avg_launch_ms, "traffic": traffic,
-                     "peak_source": pk["src"] + " bf16 sustained (kernel timed inside a long step)",
+                     "peak_source": pk["src"] + " bf16, " + peak_why,
+                     "per_gemm_tflops": {s_: round(flop_gemm / (stage_ms[s_] / 1e3) / 1e12, 1)
+                                         for s_ in GEMM_STAGES if stage_ms[s_] > 0},
                      **({"note": ("averaged over the six expert GEMMs; with few rows per expert the weight-gradient "
                                   "launches are bound by writing fp32 gradients (HBM), not by the tensor pipe "
                                   "(profiles/r01h_cfg4_wgrad.md); fc1/fc2/dgrad stages in stages_ms")}
@@ -469,6 +588,24 @@ def run_ours(args, world, rank, cfg):
     }
     if e2e is not None:
         line["e2e"] = e2e
+    if world > 1:
+        fused = bool(getattr(layer0, "ep_exchange_fused", False))
+        st = stage_ms
+        line["exchange"] = {
+            "path": ("fused: count all-gather + row stores over NVLink peer memory inside the scatter / "
+                     "fc2 / gather-combine-backward / dgrad-fc1 kernels" if fused
+                     else "transport: grouped ncclSend/ncclRecv per (peer, local expert) chunk between kernels"),
+            "fused": fused,
+            # what each profiling stage spans under expert parallelism (ep.cu)
+            "phases_ms": {"counts_and_layout (C1)": st["plan"],
+                          "scatter + global_scatter (C2, incl. waiting for the peers' rows)": st["scatter"],
+                          "fc1 + fc2 + global_gather (C3) + gather_combine": st["fc1"] + st["fc2"] + st["gather_combine"],
+                          "gather_combine_bwd + d_ys global_scatter (incl. wait)": st["gather_combine_bwd"],
+                          "backward experts + d_xs global_gather + gate": sum(st[k_] for k_ in (
+                              "dgrad_fc2", "wgrad_fc2", "db2", "dgrad_fc1", "wgrad_fc1", "db1", "gate_dwg",
+                              "gate_dx_scatter_bwd"))},
+            "nvlink_bytes_per_step_per_gpu": 4 * n * k * d * 2 * (world - 1) // world,
+        }
     pr = line["permute_roofline"]
     if world == 1 and pr["scatter_GBps"]:
         pr["scatter_frac"] = pr["scatter_GBps"] / pk["hbm"]

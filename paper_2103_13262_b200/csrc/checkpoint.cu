@@ -69,14 +69,20 @@ void Layer::load_checkpoint(const char* path) {
       shape_error("load_checkpoint: file has d_m=" + std::to_string(hd.d_m) + " d_h=" + std::to_string(hd.d_h) +
                   " experts=" + std::to_string(hd.experts) + ", the layer d_m=" + std::to_string(d) +
                   " d_h=" + std::to_string(h) + " experts=" + std::to_string(E));
+    // bf16: the weights are the rounding of fp32 masters, which the file's f64
+    // values also fill (checkpoint -> resume continues at master precision)
+    const bool masters = t == FMOE_BF16;
+    if (masters) ensure_masters();
     std::vector<double> buf((size_t)d * E);
     in.matrix(d, E, buf.data(), "gate w_g");
     upload(buf, wg, t, ctx->stream);
+    if (masters) upload(buf, m_wg, FMOE_F32, ctx->stream);
     const int64_t first = cfg.rank * el;
     for (int64_t g = 0; g < E; ++g) {
       const bool mine = g >= first && g < first + el;
       const int64_t slot = g - first;
-      auto part = [&](uint64_t rows, uint64_t cols, void* dst, fmoe_dtype as, size_t esz, const char* what) {
+      auto part = [&](uint64_t rows, uint64_t cols, void* dst, fmoe_dtype as, size_t esz, const char* what,
+                      float* master) {
         if (!mine) {
           in.matrix(rows, cols, nullptr, what);
           return;
@@ -84,16 +90,17 @@ void Layer::load_checkpoint(const char* path) {
         buf.resize(rows * cols);
         in.matrix(rows, cols, buf.data(), what);
         upload(buf, static_cast<uint8_t*>(dst) + (size_t)slot * rows * cols * esz, as, ctx->stream);
+        if (master) upload(buf, master + (size_t)slot * rows * cols, FMOE_F32, ctx->stream);
       };
-      part(d, h, w1, t, es, "expert w1");
-      part(1, h, b1, bias_t, bs, "expert b1");
-      part(h, d, w2, t, es, "expert w2");
-      part(1, d, b2, bias_t, bs, "expert b2");
+      part(d, h, w1, t, es, "expert w1", masters ? m_w1 : nullptr);
+      part(1, h, b1, bias_t, bs, "expert b1", nullptr);
+      part(h, d, w2, t, es, "expert w2", masters ? m_w2 : nullptr);
+      part(1, d, b2, bias_t, bs, "expert b2", nullptr);
     }
   } catch (const ckpt::CkptError& e) {
     rethrow(e);
   }
-  masters_fresh = false;  // bf16 training re-widens its fp32 masters
+  masters_fresh = t == FMOE_BF16;  // the masters hold the file's values (rounded once to fp32)
 }
 
 void Layer::save_checkpoint(const char* path) {
@@ -116,12 +123,19 @@ void Layer::save_checkpoint(const char* path) {
     hd.experts = E;
     hd.seed = cfg.seed;
     out.header(hd);
-    out.matrix(d, E, download(wg, (size_t)d * E, t, ctx->stream).data());
+    // a bf16 layer that trains keeps fp32 masters (SGD's state): save those, so
+    // a resumed run continues exactly where the uninterrupted one would
+    const bool masters = t == FMOE_BF16 && masters_fresh && m_wg;
+    const fmoe_dtype wt = masters ? FMOE_F32 : t;
+    const size_t ws = masters ? 4 : es;
+    const void *swg = masters ? (const void*)m_wg : wg, *sw1 = masters ? (const void*)m_w1 : w1,
+               *sw2 = masters ? (const void*)m_w2 : w2;
+    out.matrix(d, E, download(swg, (size_t)d * E, wt, ctx->stream).data());
     for (int64_t g = 0; g < E; ++g) {
       auto at = [&](const void* base, size_t n, size_t esz) { return static_cast<const uint8_t*>(base) + g * n * esz; };
-      out.matrix(d, h, download(at(w1, d * h, es), d * h, t, ctx->stream).data());
+      out.matrix(d, h, download(at(sw1, d * h, ws), d * h, wt, ctx->stream).data());
       out.matrix(1, h, download(at(b1, h, bs), h, bias_t, ctx->stream).data());
-      out.matrix(h, d, download(at(w2, h * d, es), h * d, t, ctx->stream).data());
+      out.matrix(h, d, download(at(sw2, h * d, ws), h * d, wt, ctx->stream).data());
       out.matrix(1, d, download(at(b2, d, bs), d, bias_t, ctx->stream).data());
     }
     out.close();

@@ -97,6 +97,9 @@ class Reader {
  public:
   explicit Reader(const std::string& path) : path_(path), f_(std::fopen(path.c_str(), "rb")) {
     if (!f_) throw CkptError{PROTOCOL, "checkpoint: cannot open " + path};
+    // the file length bounds every skip (fseek past EOF succeeds silently)
+    if (std::fseek(f_, 0, SEEK_END) == 0) size_ = std::ftell(f_);
+    std::fseek(f_, 0, SEEK_SET);
   }
   ~Reader() {
     if (f_) std::fclose(f_);
@@ -124,7 +127,9 @@ class Reader {
                                  std::to_string(cols)};
     const uint64_t n = rows * cols;
     if (!out) {
-      if (std::fseek(f_, (long)(8 * n), SEEK_CUR) != 0) truncated(what);
+      const long at = std::ftell(f_);
+      if (at < 0 || size_ < 0 || (uint64_t)(size_ - at) < 8 * n || std::fseek(f_, (long)(8 * n), SEEK_CUR) != 0)
+        truncated(what);
       return;
     }
     buf_.resize(8 * std::min<uint64_t>(n, kChunk));
@@ -163,6 +168,7 @@ class Reader {
   }
   std::string path_;
   FILE* f_;
+  long size_ = -1;
   std::vector<unsigned char> buf_;
 };
 

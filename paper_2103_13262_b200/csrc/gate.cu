@@ -53,6 +53,19 @@ __global__ void softmax_topk_kernel(const A* __restrict__ logits, int64_t n, int
         bv = v;
       }
     }
+    if (best < 0) {
+      // only NaN is left (a NaN logit makes the whole row NaN): the
+      // reference's stable sort keeps column order, so take the lowest column
+      // not chosen yet -- indices always stay in [0, e)
+      for (int c = 0; c < e && best < 0; ++c) {
+        bool used = false;
+        for (int q = 0; q < j; ++q) used |= idx[i * k + q] == c;
+        if (!used) {
+          best = c;
+          bv = s[c];
+        }
+      }
+    }
     idx[i * k + j] = best;
     vals[i * k + j] = bv;
     pv = bv;

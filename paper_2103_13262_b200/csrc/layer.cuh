@@ -47,6 +47,7 @@ struct Layer {
   double* t_loss = nullptr;
   float *m_wg = nullptr, *m_w1 = nullptr, *m_w2 = nullptr;
   bool masters_fresh = false;
+  void ensure_masters();
   // expert parallelism (ep.cu)
   struct Ep;
   Ep* ep = nullptr;

@@ -45,10 +45,9 @@ __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
 // kernel on this stream (the producer) has completed, so its stores -- local
 // and remote -- are performed before this kernel runs.
 __global__ void signal_kernel(void* const* flags, int W, int r, int phase, uint32_t epoch) {
-  const int p = threadIdx.x;
-  if (p < W) {
+  __threadfence_system();
+  for (int p = threadIdx.x; p < W; p += blockDim.x) {  // any world size
     uint32_t* f = reinterpret_cast<uint32_t*>(flags[p]) + phase * W + r;
-    __threadfence_system();
     st_release_sys(f, epoch);
   }
 }

@@ -182,6 +182,7 @@ __global__ void plan_rank(const int32_t* __restrict__ idx, int64_t nk, int k, in
     int before = 0;
     if (key >= 0) before = run[key];
     __syncwarp();
+    if (key < 0 && f < nk) inverse_pos[f] = 0;  // flagged by plan_hist; keep later reads in bounds
     if (key >= 0) {
       const int pos = bases[t] + before + __popc(peers & lt);
       const int i = (int)(f / k);

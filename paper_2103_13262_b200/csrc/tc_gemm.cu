@@ -338,9 +338,12 @@ __device__ __forceinline__ void epi_gate64(const Params& p, uint32_t tbase, int 
     for (int i = 0; i < 64; ++i) {
       if (i < E) {
         const float s = ev[i];
-        if (s > v0) {
+        // an empty slot takes any value, so a NaN row (every score NaN, the
+        // reference's stable sort leaves it in column order) still selects
+        // valid experts 0, 1 with NaN scores instead of leaving -1
+        if (s > v0 || i0 < 0) {
           v1 = v0; i1 = i0; v0 = s; i0 = i;
-        } else if (s > v1) {
+        } else if (s > v1 || i1 < 0) {
           v1 = s; i1 = i;
         }
       }
@@ -368,7 +371,7 @@ __device__ __forceinline__ void epi_gate64(const Params& p, uint32_t tbase, int 
 #pragma unroll
       for (int j = 0; j < KMAX; ++j) {
         if (j < k) {
-          const bool take = carry || (cs > tv[j]);
+          const bool take = carry || (cs > tv[j]) || ti[j] < 0;  // empty slots take NaN too
           if (take) {
             const float tf = tv[j];
             const int tix = ti[j];
@@ -441,7 +444,7 @@ __device__ __forceinline__ void epi_gate(const Params& p, uint32_t tbase, int ro
 #pragma unroll
         for (int j = 0; j < KMAX; ++j) {
           if (j < k) {
-            const bool take = carry || (cs > tv[j]);
+            const bool take = carry || (cs > tv[j]) || ti[j] < 0;  // empty slots take NaN too
             if (take) {
               const float tf = tv[j];
               const int tix = ti[j];

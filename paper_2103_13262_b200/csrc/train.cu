@@ -12,6 +12,7 @@
 #include <type_traits>
 #include <vector>
 
+#include "comm.cuh"
 #include "layer.cuh"
 #include "ops.cuh"
 
@@ -132,10 +133,33 @@ void Layer::sgd(void* param, float* master, const void* grad, int64_t n, double 
   CK_LAUNCH(ctx);
 }
 
+// fp32 master copies of the bf16 weights (SGD updates them; the bf16 weights
+// are their rounding).  Allocated on the first train_step or checkpoint load.
+void Layer::ensure_masters() {
+  if (t != FMOE_BF16 || m_wg) return;
+  const int64_t d = cfg.d_m, h = cfg.d_h, el = cfg.n_e_local;
+  auto grab = [&](size_t bytes) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+    owned.push_back(p);
+    return (float*)p;
+  };
+  m_wg = grab((size_t)d * E * 4);
+  m_w1 = grab((size_t)el * d * h * 4);
+  m_w2 = grab((size_t)el * h * d * 4);
+}
+
 double Layer::train_step(const void* x, const void* target, double lr) {
   const int64_t n = cfg.n_b * cfg.d_m, el = cfg.n_e_local, d = cfg.d_m, h = cfg.d_h;
   const int W = (int)cfg.world_size;
   const bool ep = W > 1;
+  // the gate gradient is all-reduced over the world (param_sync.cpp:46-61):
+  // an expert-parallel step needs the transport for it, so refuse before any
+  // forward/backward work or gradient scaling is issued
+  if (ep && (!ctx->transport || ctx->transport->world != W || ctx->transport->rank != cfg.rank))
+    protocol_error("train_step: expert-parallel training (world " + std::to_string(W) +
+                   ") needs a transport of the same world and rank for the gate all-reduce: "
+                   "fmoe_comm_init, fmoe_comm_attach or fmoe_ctx_join_world");
   if (!t_y) {  // buffers for the step, allocated on first use
     auto grab = [&](size_t bytes) {
       void* p = nullptr;
@@ -147,12 +171,8 @@ double Layer::train_step(const void* x, const void* target, double lr) {
     t_dy = grab((size_t)n * es);
     t_dx = grab((size_t)n * es);
     t_loss = (double*)grab((kLossBlocks + 2) * sizeof(double));
-    if (t == FMOE_BF16) {
-      m_wg = (float*)grab((size_t)d * E * 4);
-      m_w1 = (float*)grab((size_t)el * d * h * 4);
-      m_w2 = (float*)grab((size_t)el * h * d * 4);
-    }
   }
+  ensure_masters();
   if (t == FMOE_BF16 && !masters_fresh) {  // fp32 masters widened from the current bf16 weights
     widen_kernel<<<blocks_for(d * E), 256, 0, ctx->stream>>>((const __nv_bfloat16*)wg, m_wg, d * E);
     widen_kernel<<<blocks_for(el * d * h), 256, 0, ctx->stream>>>((const __nv_bfloat16*)w1, m_w1, el * d * h);

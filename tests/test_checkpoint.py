@@ -114,3 +114,41 @@ def test_shape_mismatch(fm, orc, ref, tmp_path):
         layer.load_checkpoint(path)
     with pytest.raises(fm.ProtocolError):
         layer.load_checkpoint(str(tmp_path / "missing.ckpt"))
+
+
+@pytest.mark.gpu
+def test_truncated_file_fails_on_every_rank(fm, orc, ref, tmp_path):
+    """A rank whose own experts precede the cut still rejects the file, as the
+    reference loader does (the skipped experts are checked against the length)."""
+    d, h, el, world, k = 16, 32, 2, 2, 2
+    w = orc.init_state(3, d, h, el * world)
+    path = tmp_path / "full.ckpt"
+    ref.save_checkpoint(str(path), w, n_b=8, k=k, seed=3)
+    cut = tmp_path / "cut.ckpt"
+    cut.write_bytes(path.read_bytes()[:-8 * (h * d)])  # the last expert's w2 is short
+    for r in range(world):
+        layer = fm.MoELayer(fm.MoEConfig(8, d, h, k, el, world, 3), rank=r, dtype=torch.float64)
+        with pytest.raises(fm.ProtocolError):
+            layer.load_checkpoint(str(cut))
+
+
+@pytest.mark.gpu
+def test_bf16_training_resumes_from_fp32_masters(fm, tmp_path):
+    """bf16 training updates fp32 masters; a checkpoint keeps them, so a run
+    resumed from the file continues bit for bit like the uninterrupted one."""
+    n, d, h, e, k, lr = 256, 64, 128, 8, 2, 0.05
+    g = torch.Generator().manual_seed(4)
+    xs = [torch.rand(n, d, generator=g).bfloat16().cuda() for _ in range(5)]
+    ts = [torch.rand(n, d, generator=g).bfloat16().cuda() for _ in range(5)]
+    a = fm.MoELayer(fm.MoEConfig(n, d, h, k, e, 1, 21), dtype=torch.bfloat16)
+    for i in range(3):
+        a.train_step(xs[i], ts[i], lr)
+    path = str(tmp_path / "bf.ckpt")
+    a.save_checkpoint(path)
+    b = fm.MoELayer(fm.MoEConfig(n, d, h, k, e, 1, 0), dtype=torch.bfloat16)
+    b.load_checkpoint(path)
+    for i in range(3, 5):
+        la, lb = a.train_step(xs[i], ts[i], lr), b.train_step(xs[i], ts[i], lr)
+        assert la == lb
+    for key, v in _weights(a).items():
+        assert v.tobytes() == _weights(b)[key].tobytes(), key

@@ -62,3 +62,33 @@ def test_top8_of_64(fm, orc):
 
 def test_more_than_256_experts(fm, orc):
     _run(fm, orc, 2048, 64, 64, 512, 2, check_grads=False)
+
+
+@pytest.mark.parametrize("dtype,e,k", [(torch.bfloat16, 16, 2), (torch.bfloat16, 64, 3), (torch.bfloat16, 128, 2),
+                                       (torch.bfloat16, 512, 2), (torch.float64, 16, 2), (torch.float32, 16, 3)])
+def test_nan_token_row_routes_like_the_reference(fm, orc, dtype, e, k):
+    """A NaN in one token makes that row's softmax all-NaN; the reference's
+    stable sort then keeps column order (matrix.cpp:172-189), so the row picks
+    experts 0..k-1 with NaN scores.  Every index stays in [0, E), the NaN stays
+    in its own row, and the other rows equal a run where that row is finite."""
+    n, d, h, seed, bad = 300, 64, 64, 11, 5
+    x = bf16_round(orc.seeded_matrix(seed, 102, n, d))
+    dy = bf16_round(orc.seeded_matrix(seed, 103, n, d))
+    xn = x.copy()
+    xn[bad, 7] = np.nan
+    outs = []
+    for xi in (xn, x):
+        layer = fm.MoELayer(fm.MoEConfig(n, d, h, k, e, 1, seed), dtype=dtype)
+        y = layer.forward(dev(xi, dtype))
+        dx = layer.backward(dev(dy, dtype))
+        torch.cuda.synchronize()
+        outs.append((host(layer.routing()[0]).astype(np.int64), host(y), host(dx)))
+    (idx, y, dx), (idx0, y0, dx0) = outs
+    assert ((idx >= 0) & (idx < e)).all()
+    assert (idx[bad] == np.arange(k)).all()
+    assert np.isnan(y[bad]).all()
+    keep = np.ones(n, bool)
+    keep[bad] = False
+    assert (idx[keep] == idx0[keep]).all()
+    assert np.array_equal(y[keep], y0[keep])
+    assert np.isfinite(y[keep]).all()
