@@ -487,7 +487,7 @@ def run_ours(args, world, rank, cfg):
                 layer0.forward(xb[i & 1], y)
                 layer0.backward(dy, dx)
                 used[i & 1].record(stream)
-                torch.sum(y, dtype=torch.float32, out=res_d[i])
+                torch.sum(y, dim=(0, 1), dtype=torch.float32, out=res_d[i])
                 res_h[i].copy_(res_d[i], non_blocking=True)
             t1_.record(stream)
             torch.cuda.synchronize()

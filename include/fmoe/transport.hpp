@@ -13,8 +13,11 @@
 #include <chrono>
 #include <cstdint>
 #include <memory>
+#include <span>
 #include <string>
 #include <vector>
+
+#include "fmoe/wire.hpp"
 
 struct fmoe_ctx;  // include/fmoe_b200.h
 
@@ -26,6 +29,10 @@ class Transport {
   virtual int rank() const = 0;
   virtual int world_size() const = 0;
   virtual void barrier() = 0;
+  // Framed byte messages (transport.hpp:25-30 of the reference) are not how
+  // the drop-in moves data: both throw TransportError (see fmoe/wire.hpp).
+  virtual void send_frame(int peer, MsgType type, std::uint32_t tag, std::span<const std::byte> payload);
+  virtual std::vector<std::byte> recv_frame(int peer, MsgType expected_type, std::uint32_t expected_tag);
   // C-ABI context (device, stream, communicator) the collectives run on.
   virtual fmoe_ctx* device_context() const = 0;
   // Per-transport collective counter (transport.hpp:34 of the reference).
@@ -62,6 +69,8 @@ struct HostPort {
   std::uint16_t port = 0;
 };
 std::vector<HostPort> localhost_endpoints(int world_size, std::uint16_t base_port);
+// TCP rendezvous configuration: not provided by the B200 drop-in (throws TransportError).
+std::vector<HostPort> parse_hostfile(const std::string& path);
 // Not provided by the B200 drop-in: throws TransportError (use nccl_connect).
 std::unique_ptr<Transport> tcp_connect(int rank, const std::vector<HostPort>& endpoints,
                                        std::chrono::milliseconds timeout = std::chrono::seconds(30));

@@ -2,7 +2,7 @@
 drop-in (include/fmoe/*.hpp + libfmoe_dropin.so over the C-ABI).
 
 tests/dropin/Makefile builds proj/tests/test_{tensor,gate,dispatch,expert,
-moe_layer}.cpp from the reference checkout with a minimal doctest stand-in
+moe_layer,comm,param_sync}.cpp from the reference checkout with a minimal doctest stand-in
 (tests/dropin/doctest.h); the binaries travel to the GPU box with the
 snapshot.  Every operator they call runs on the GPU in the FMOE_F64 parity mode.
 
@@ -17,8 +17,15 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "tests", "dropin", "_bin")
 LIB = os.path.join(ROOT, "paper_2103_13262_b200", "libfmoe_dropin.so")
-SUITES = ["test_tensor", "test_gate", "test_dispatch", "test_expert", "test_moe_layer"]
-EXCLUDE = {}
+SUITES = ["test_tensor", "test_gate", "test_dispatch", "test_expert", "test_moe_layer", "test_comm",
+          "test_param_sync"]
+# test_comm.cpp's wire-codec and TCP cases (lines 17-86, 297-395) exercise the
+# reference's framed-byte transport, which the B200 drop-in does not have (rows
+# move over NCCL / device copies; SURVEY §2, §8 put the codec and TCP out of
+# scope).  They are skipped on both libraries; every exchange_counts,
+# all_to_all_rows(_reverse) and allreduce_sum case runs.
+EXCLUDE = {"test_comm": ["frame encoding", "frame decoding", "row payloads survive the wire",
+                         "detects shape mismatch", "tcp transport", "tcp rendezvous", "hostfile parsing"]}
 
 
 def test_dropin_library_exports_reference_api():
@@ -66,5 +73,5 @@ def test_reference_unit_tests_pass_on_dropin(suite):
     assert summary, out[-3000:]
     assert (cases, checks) == (rcases, rchecks), out[-3000:]
     assert rc == rrc
-    if suite != "test_tensor":
+    if suite not in ("test_tensor", "test_comm"):  # the reference fails test_tensor.cpp:42,51,56, test_comm.cpp:119
         assert rc == 0 and "0 failed" in summary[0], out[-3000:]
