@@ -17,10 +17,6 @@ void* ctx_workspace(Ctx* ctx, size_t bytes);
 
 namespace {
 
-__global__ void fill_split_offsets(int32_t* off, int64_t n_splits, int64_t rows_per_split, int64_t n) {
-  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s <= n_splits) off[s] = (int32_t)std::min<int64_t>(s * rows_per_split, n);
-}
 
 __global__ void cast_f32_bf16(const float* __restrict__ in, __nv_bfloat16* __restrict__ out, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -122,14 +118,11 @@ void gate_dwg_bf16(Ctx* ctx, const void* x, const __nv_bfloat16* dz, int64_t n, 
   }
   const int64_t S = gate_dwg_splits(n);
   const int64_t per = ceil_div(ceil_div(n, S), 64) * 64;
-  int32_t* offs = reinterpret_cast<int32_t*>(part_ws + S * d * e);
-  fill_split_offsets<<<1, 64, 0, ctx->stream>>>(offs, S, per, n);
-  CK_LAUNCH(ctx);
   const CUtensorMap ta = tc::make_tmap(x, d, n, d * 2, 64, 64);   // x^T: MN-major
   const CUtensorMap tb = tc::make_tmap(dz, e, n, e * 2, 64, 64);  // dz: MN-major
   tc::Params p{};
   p.mode = tc::RAGGED_K;
-  p.M = (int)d; p.N = (int)e; p.n_groups = (int)S; p.k_offsets = offs;
+  p.M = (int)d; p.N = (int)e; p.K = (int)n; p.n_groups = (int)S; p.k_split = (int)per;  // split s: rows [s*per, ...)
   p.epi = tc::EPI_F32; p.C = part_ws; p.ldc = e; p.c_group_stride = d * e;
   const int bn = pick_bn(e);
   tc::launch(ctx, bn, true, true, ta, tb, p, S * ceil_div(d, 128) * ceil_div(e, bn));
@@ -320,7 +313,6 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
   const int cg = pair_mode(b);
   const int64_t cap = b.capacity;
   const int64_t max_tiles = cap / (128 * cg);  // (pair) row tiles
-  const int64_t t128 = cap / 128;              // 128-row tiles (bias partials)
   const bool do_dgrad = phase != EXPERTS_BWD_WGRAD, do_wgrad = phase != EXPERTS_BWD_DGRAD;
   if (do_dgrad) {  // dgrad fc2: d_pre = (d_ys W2^T) * (hidden > 0); B(k=c, n=j) = W2[e][j][c] -> K-major [E*h, d]
     const CUtensorMap ta = tc::make_tmap(d_ys, d, cap, d * 2, 64, 128);
@@ -329,7 +321,6 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     p.mode = tc::RAGGED_M; p.M = (int)cap; p.N = (int)h; p.K = (int)d;
     p.tile_group = b.tile_expert; p.n_mtiles = b.n_tiles; p.b_group_rows = (int)h;
     p.epi = tc::EPI_MASK_BF16; p.C = d_pre; p.ldc = h; p.mask = (const __nv_bfloat16*)hidden; p.ldm = h;
-    p.colsum_part = part_ws;  // d_b1 = colsum(d_pre) fused into the epilogue (expert.cpp:51-53)
     p.relu_bits = relu_bits;  // 1 bit per activation instead of re-reading hidden
     tc::launch(ctx, 256, false, false, ta, tb, p, max_tiles * ceil_div(h, 256), cg);
     ctx_mark(ctx, MARK_DGRAD2);
@@ -347,14 +338,10 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     p.mode = tc::RAGGED_K; p.M = (int)h; p.N = (int)d; p.n_groups = (int)E; p.k_offsets = b.offsets;
     p.group_order = group_order;
     p.epi = tc::EPI_F32; p.C = g.d_w2; p.ldc = d; p.c_group_stride = h * d;
+    // d_b2 = colsum(d_ys) per expert (expert.cpp:43-45) from the B tiles this GEMM streams
+    p.bsum_out = (float*)g.d_b2; p.bsum_group_stride = d;
     tc::launch(ctx, 256, true, true, ta, tb, p, E * ceil_div(h, 128 * cg) * ceil_div(d, 256), cg);
     ctx_mark(ctx, MARK_WGRAD2);
-  }
-  // d_b2 = colsum(d_ys) per expert (expert.cpp:43-45): tile partials + ordered reduce
-  float* part_b2 = part_ws + t128 * h;
-  if (do_wgrad) {
-    tile_colsum(ctx, (const __nv_bfloat16*)d_ys, d, b.n_tiles, t128, part_b2);
-    reduce_tile_partials(ctx, part_b2, d, b.offsets, E, (float*)g.d_b2);
     ctx_mark(ctx, MARK_DB2);
   }
   if (do_dgrad) {  // dgrad fc1: d_xs = d_pre W1^T; B(k=j, n=c) = W1[e][c][j] -> K-major [E*d, h]
@@ -375,11 +362,10 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     p.mode = tc::RAGGED_K; p.M = (int)d; p.N = (int)h; p.n_groups = (int)E; p.k_offsets = b.offsets;
     p.group_order = group_order;
     p.epi = tc::EPI_F32; p.C = g.d_w1; p.ldc = h; p.c_group_stride = d * h;
+    // d_b1 = colsum(d_pre) per expert (expert.cpp:51-53) from the B tiles this GEMM streams
+    p.bsum_out = (float*)g.d_b1; p.bsum_group_stride = h;
     tc::launch(ctx, 256, true, true, ta, tb, p, E * ceil_div(d, 128 * cg) * ceil_div(h, 256), cg);
     ctx_mark(ctx, MARK_WGRAD1);
-  }
-  if (do_wgrad) {  // d_b1 partials come from the dgrad-fc2 epilogue
-    reduce_tile_partials(ctx, part_ws, h, b.offsets, E, (float*)g.d_b1);
     ctx_mark(ctx, MARK_DB1);
   }
 }

@@ -55,6 +55,7 @@ struct Params {
   const int* tile_group;     // RAGGED_M: group of each 128-row tile (NULL: all group 0)
   const int* n_mtiles;       // RAGGED_M: device count of valid row tiles (NULL: ceil(M/128))
   const int* k_offsets;      // RAGGED_K: [G+1] K-row range of each group (multiples of 64)
+  int k_split;               // RAGGED_K without k_offsets: group g = rows [g*k_split, min(K, (g+1)*k_split))
   // RAGGED_K (optional): groups in decreasing K-length; tiles are then dealt
   // to the persistent CTAs heaviest first in a snake (boustrophedon) order so
   // skewed expert sizes (Zipf routing) stay balanced across SMs
@@ -79,16 +80,19 @@ struct Params {
   const __nv_bfloat16* gather_src;  // d_xs [rows][N]
   const int* inverse_pos;           // [M][gk]
   int gk;
-  // optional fused column sums of the epilogue values (RAGGED_M bf16
-  // epilogues): colsum_part[m_tile][N] = sum over the tile's 128 rows, fp32
-  // (bias gradients without re-reading the activation; reduced per expert
-  // by reduce_tile_partials in a fixed order -> deterministic)
-  float* colsum_part;
   // relu bitmaps [rows][N/32]: written by the fc1 epilogue (bit = value > 0),
   // read by the dgrad-fc2 epilogue instead of the bf16 activations (64 MiB
   // instead of 1 GiB at cfg2)
   uint32_t* relu_bits_out;
   const uint32_t* relu_bits;
+  // optional column sums of the B operand over each group's K range
+  // (RAGGED_K weight gradients with an MN-major B: B = d_ys / d_pre, whose
+  // per-expert column sums are the bias gradients d_b2 / d_b1, expert.cpp:
+  // 43-45, 51-53).  Warps 2 and 3 sum the B tiles the MMAs have consumed on
+  // the tiles of M-tile 0 and write bsum_out[g * bsum_group_stride + n] once
+  // per (group, column) in a fixed order: no extra pass over B, no atomics.
+  float* bsum_out;
+  int64_t bsum_group_stride;
   int tma_out;  // set by launch(): outputs leave through TMA stores
   // Expert parallelism over peer memory (EPI_BF16, RAGGED_M): every output row
   // is stored straight into the rank that sent it (fused global_gather,
