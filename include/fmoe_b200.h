@@ -63,6 +63,15 @@ int64_t fmoe_ctx_launches(const fmoe_ctx* ctx);
  * 16 gate d_x + scatter_backward. */
 int fmoe_ctx_profile(fmoe_ctx* ctx, int n_steps);
 int fmoe_ctx_profile_read(fmoe_ctx* ctx, float* stage_ms, int n_stages, int* steps_done);
+/* Effective SM clock of the expert GEMMs: arm max_launches probe slots
+ * (0 disarms); every expert-GEMM launch then records clock64 / globaltimer at
+ * the start and end of its first CTA.  probe_read synchronises and returns the
+ * cycle-weighted clock over the recorded launches (MHz = sum of cycles / sum
+ * of nanoseconds * 1e3) and how many launches were recorded.  Lets a caller
+ * state the tensor roofline at the clock the kernels actually ran at (the
+ * power-capped B200 runs dense GEMMs well below clocks.max.sm). */
+int fmoe_ctx_clock_probe(fmoe_ctx* ctx, int max_launches);
+int fmoe_ctx_clock_probe_read(fmoe_ctx* ctx, double* sm_mhz, int* launches);
 /* Synchronise the stream and surface any deferred device-side error (e.g. an
  * out-of-range expert index seen by fmoe_plan_build). */
 int fmoe_ctx_check(fmoe_ctx* ctx);

@@ -1,3 +1,4 @@
+#include <vector>
 // capi.cu -- the extern "C" boundary (include/fmoe_b200.h): context, operator
 // entry points and status/error mapping.  Internal exceptions never cross it.
 #include <cstring>
@@ -84,6 +85,7 @@ int fmoe_ctx_destroy(fmoe_ctx* ctx) {
   FMOE_GUARD({
     Ctx* c = C(ctx);
     cudaFree(c->d_error);
+    if (c->d_probe) cudaFree(c->d_probe);
     if (c->ws) cudaFree(c->ws);
     if (c->copy_in) cudaStreamDestroy(c->copy_in);
     if (c->copy_out) cudaStreamDestroy(c->copy_out);
@@ -138,6 +140,42 @@ int fmoe_ctx_profile_read(fmoe_ctx* ctx, float* stage_ms, int n_stages, int* ste
         stage_ms[i] += ms;
       }
     if (steps_done) *steps_done = p->used;
+  })
+}
+
+int fmoe_ctx_clock_probe(fmoe_ctx* ctx, int max_launches) {
+  FMOE_GUARD({
+    Ctx* c = C(ctx);
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->d_probe) cudaFree(c->d_probe);
+    c->d_probe = nullptr;
+    c->probe_cap = c->probe_next = 0;
+    if (max_launches > 0) {
+      CK(cudaMalloc(&c->d_probe, (size_t)max_launches * 4 * 8));
+      CK(cudaMemset(c->d_probe, 0, (size_t)max_launches * 4 * 8));
+      c->probe_cap = max_launches;
+    }
+  })
+}
+
+int fmoe_ctx_clock_probe_read(fmoe_ctx* ctx, double* sm_mhz, int* launches) {
+  FMOE_GUARD({
+    Ctx* c = C(ctx);
+    if (!c->d_probe) shape_error("clock probe not armed");
+    CK(cudaStreamSynchronize(c->stream));
+    std::vector<unsigned long long> v((size_t)c->probe_next * 4);
+    if (!v.empty()) CK(cudaMemcpy(v.data(), c->d_probe, v.size() * 8, cudaMemcpyDeviceToHost));
+    double cyc = 0.0, ns = 0.0;
+    int n = 0;
+    for (int i = 0; i < c->probe_next; ++i) {
+      const unsigned long long* q = v.data() + 4 * i;
+      if (q[2] <= q[0] || q[3] <= q[1]) continue;
+      cyc += (double)(q[2] - q[0]);
+      ns += (double)(q[3] - q[1]);
+      ++n;
+    }
+    if (sm_mhz) *sm_mhz = ns > 0 ? cyc / ns * 1e3 : 0.0;
+    if (launches) *launches = n;
   })
 }
 

@@ -73,7 +73,17 @@ struct Ctx {
   // their own streams so PCIe transfers overlap the layer's kernels
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
   cudaEvent_t ev_io[4] = {nullptr, nullptr, nullptr, nullptr};
+  // SM clock probe of the expert GEMMs (fmoe_ctx_clock_probe): per launch,
+  // CTA 0 records (clock64, globaltimer) at its start and end
+  unsigned long long* d_probe = nullptr;
+  int probe_cap = 0, probe_next = 0;
 };
+
+// Next clock-probe slot (4 u64) of the context, or NULL when not armed / full.
+inline unsigned long long* ctx_probe_slot(Ctx* c) {
+  if (!c->d_probe || c->probe_next >= c->probe_cap) return nullptr;
+  return c->d_probe + 4 * (c->probe_next++);
+}
 
 inline void ctx_mark(Ctx* c, int id) {
   Prof* p = c->prof;

@@ -19,6 +19,7 @@
 //     into its final slot (C2) -> experts -> reverse exchange (C3) ->
 //     gather_combine; backward on the same routes.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -56,6 +57,15 @@ struct Layer::Ep {
   void** peer_table = nullptr;  // [PB_N][W] device pointer tables
   bool fused = false;           // the current step runs the fused path
   bool device_plan = false;     // its layouts were computed on the device
+  // overlapped exchange (cross-process peers): the rows are pushed by a
+  // concurrent kernel on `side` while fc1 / dgrad fc2 consume them tile by
+  // tile as their chunks are published (per-chunk flags after the PH_N phase
+  // flags in `flags`: [dir][el][W])
+  bool overlap = false;         // the current step overlaps the exchange
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_go = nullptr, ev_pushed = nullptr;
+  int32_t* push_ctr = nullptr;  // [1 + E]: work-unit counter, rows done per send segment
+  int32_t* mtile_order = nullptr;
 };
 
 namespace {
@@ -101,8 +111,10 @@ void Layer::ep_alloc() {
   if (t == FMOE_BF16) relu_bits = (uint32_t*)alloc(owned, cap * (h / 32) * 4);
   const int64_t W = P.W;
   P.cnt_mat = (int32_t*)alloc(owned, W * E * 4);
-  P.flags = (uint32_t*)alloc(owned, PH_N * W * 4);
-  CK(cudaMemset(P.flags, 0, PH_N * W * 4));
+  P.flags = (uint32_t*)alloc(owned, (PH_N * W + 2 * P.el * W) * 4);
+  CK(cudaMemset(P.flags, 0, (PH_N * W + 2 * P.el * W) * 4));
+  P.push_ctr = (int32_t*)alloc(owned, (1 + E) * 4);
+  P.mtile_order = (int32_t*)alloc(owned, (cap / 128 + 2) * 4);
   P.g_rank = (int32_t*)alloc(owned, E * 4);
   P.g_delta = (int64_t*)alloc(owned, E * 8);
   P.rt = (int32_t*)alloc(owned, 3 * P.el * W * 4);
@@ -378,6 +390,134 @@ __global__ void ep_zero_pads_kernel(uint8_t* __restrict__ buf, int64_t row_bytes
   }
 }
 
+// Row tiles of the receive layout in the order their rows are expected to
+// land under the overlapped exchange: sender s pushes to destinations s, s+1,
+// ... (mod W) and, per destination, its experts in order, so chunk (e, s)
+// reaches this rank r in slot q = (r - s) mod W (q = 0: this rank's own rows).
+// A tile's key is the latest (q, e) among the chunks it covers; tiles are
+// dealt in increasing key (counting sort; order inside a key is arbitrary --
+// it only changes which CTA computes a tile, never its value).
+__global__ void ep_tile_order_kernel(const int32_t* __restrict__ rt, const int32_t* __restrict__ tile_expert,
+                                     const int32_t* __restrict__ n_tiles, int W, int el, int r, int cg,
+                                     int32_t* __restrict__ order) {
+  extern __shared__ int32_t cnt[];  // [W*el] counts, then cursors
+  const int K = W * el, C = el * W;
+  const int nt = *n_tiles / cg;
+  for (int i = threadIdx.x; i < K; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  auto key_of = [&](int t) {
+    const int e = tile_expert[t * cg];
+    const int r0 = t * 128 * cg, r1 = r0 + 128 * cg;
+    int key = 0;
+    for (int s = 0; s < W; ++s) {
+      const int st = rt[e * W + s], nr = rt[C + e * W + s];
+      if (nr > 0 && st < r1 && st + nr > r0) key = max(key, ((r - s + W) % W) * el + e);
+    }
+    return key;
+  };
+  for (int t = threadIdx.x; t < nt; t += blockDim.x) atomicAdd(&cnt[key_of(t)], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int i = 0; i < K; ++i) {
+      const int c = cnt[i];
+      cnt[i] = acc;
+      acc += c;
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nt; t += blockDim.x) order[atomicAdd(&cnt[key_of(t)], 1)] = t;
+}
+
+__device__ __forceinline__ void st_release_sys_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// The overlapped global scatter: this rank's send rows, destination-major (the
+// send layout is grouped by destination rank, then its local expert,
+// collectives.cpp:114-122), pushed into every rank's receive buffer in the
+// rotated order s, s+1, ... so each destination hears from one sender at a
+// time.  Work units of kUnit rows are taken in that order from an atomic
+// counter; when the last unit of send segment g (destination p, its expert e)
+// is stored, the CTA that completed it publishes flag [e][r] in p's memory
+// (fence + release store after the block barrier, the grid-sync pattern).
+// SCALE (backward): d_ys = bf16(w * d_y), the same rounding as gcb_kernel.
+constexpr int kPushUnit = 128;
+constexpr int kPushThreads = 512;
+template <bool SCALE>
+__global__ void __launch_bounds__(kPushThreads) ep_push_kernel(
+    const __nv_bfloat16* __restrict__ src, int64_t d, fmoe_plan p, const float* __restrict__ w,
+    void* const* dst, const int64_t* __restrict__ g_delta, void* const* flags, int flag_base, int W, int r, int el,
+    uint32_t epoch, int32_t* __restrict__ ctr) {
+  extern __shared__ int32_t sh[];  // [E+1] unit prefix in rotated segment order, + broadcast slot
+  const int E = W * el;
+  int32_t* pref = sh;
+  int32_t* slot = sh + E + 1;
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int q = 0; q < E; ++q) {
+      const int g = ((r + q / el) % W) * el + q % el;
+      pref[q] = acc;
+      acc += (p.offsets[g + 1] - p.offsets[g] + kPushUnit - 1) / kPushUnit;
+    }
+    pref[E] = acc;
+  }
+  __syncthreads();
+  const int total = pref[E];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n16 = d / 8;  // 16-byte vectors per row
+  while (true) {
+    if (threadIdx.x == 0) *slot = atomicAdd(ctr, 1);
+    __syncthreads();
+    const int u = *slot;
+    __syncthreads();
+    if (u >= total) break;
+    int lo = 0, hi = E;  // segment q with pref[q] <= u < pref[q+1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (pref[mid] <= u) lo = mid; else hi = mid;
+    }
+    const int q = lo;
+    const int dp = (r + q / el) % W, e = q % el, g = dp * el + e;
+    const int seg0 = p.offsets[g], seg1 = p.offsets[g + 1];
+    const int a = seg0 + (u - pref[q]) * kPushUnit, b = min(seg1, a + kPushUnit);
+    uint8_t* out = static_cast<uint8_t*>(dst[dp]);
+    const int64_t delta = g_delta[g];
+    for (int pos = a + warp; pos < b; pos += kPushThreads / 32) {
+      const int i = __ldg(p.src_row + pos);
+      const uint4* s4 = reinterpret_cast<const uint4*>(src + (int64_t)i * d);
+      uint4* d4 = reinterpret_cast<uint4*>(out + (pos + delta) * d * 2);
+      float wv = 1.f;
+      if constexpr (SCALE) wv = __ldg(w + (int64_t)i * p.k + __ldg(p.slot + pos));
+      for (int64_t c = lane; c < n16; c += 32 * 4) {
+        uint4 v[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (c + 32 * t < n16) v[t] = __ldg(s4 + c + 32 * t);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          if (c + 32 * t >= n16) break;
+          if constexpr (SCALE) {
+            __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(&v[t]);
+#pragma unroll
+            for (int z = 0; z < 8; ++z) h[z] = __float2bfloat16_rn(wv * __bfloat162float(h[z]));
+          }
+          d4[c + 32 * t] = v[t];
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      const int n = b - a;
+      if (atomicAdd(ctr + 1 + g, n) + n == seg1 - seg0) {
+        __threadfence_system();
+        st_release_sys_u32(static_cast<uint32_t*>(flags[dp]) + flag_base + e * W + r, epoch);
+      }
+    }
+  }
+}
+
 static size_t ep_layout_smem(int W, int64_t el) {
   const int64_t E = W * el;
   return (size_t)(W * E + W * el * W + el + 1) * 4;
@@ -395,6 +535,11 @@ static void ep_plan_peer_device(Layer& L) {
   ep_layout_kernel<<<1, 256, ep_layout_smem(W, el), ctx->stream>>>(
       P.cnt_mat, W, (int)el, (int)P.align, P.r, P.g_rank, P.g_delta, P.rt, P.rplan.counts, P.rplan.offsets,
       P.rplan.tile_expert, P.rplan.n_tiles);
+  CK_LAUNCH(ctx);
+  // the order the overlapped exchange deals row tiles in (harmless otherwise)
+  const int cg = P.align % 256 == 0 ? 2 : 1;
+  ep_tile_order_kernel<<<1, 1024, (size_t)E * 4, ctx->stream>>>(P.rt, P.rplan.tile_expert, P.rplan.n_tiles, W,
+                                                                 (int)el, P.r, cg, P.mtile_order);
   CK_LAUNCH(ctx);
   (void)C;
   P.planned = true;
@@ -472,6 +617,72 @@ static Transport* ep_transport(const Layer& L) {
 
 void Layer::ep_check() const { ep_transport(*this); }
 
+// SMs the concurrent push keeps while fc1 / dgrad fc2 run beside it
+#ifndef FMOE_EP_PUSH_SMS
+#define FMOE_EP_PUSH_SMS 16
+#endif
+
+// The overlapped exchange needs device layouts, bf16 rows, and peers in other
+// processes (a kernel spinning on a flag must not be able to starve the kernel
+// that releases it, which ranks sharing one process and GPU could);
+// FMOE_EP_OVERLAP=0 keeps the phase-ordered fused exchange.
+static bool ep_overlap_ok(const Layer& L) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("FMOE_EP_OVERLAP");
+    return !(e && e[0] == '0');
+  }();
+  const Layer::Ep& P = *L.ep;
+  return enabled && P.fused && P.device_plan && P.peer.cross_process && !P.peer.lw && L.t == FMOE_BF16 &&
+         L.cfg.d_m % 8 == 0 && L.ctx->num_sms > 2 * FMOE_EP_PUSH_SMS;
+}
+
+// dir 0: forward rows (x -> peers' xs), 1: backward (w * d_y -> peers' d_ys)
+static Arrival ep_arrival(const Layer& L, int dir) {
+  const Layer::Ep& P = *L.ep;
+  Arrival a;
+  a.flags = P.flags + PH_N * P.W + dir * P.el * P.W;
+  a.epoch = P.peer.epoch;
+  a.rt = P.rt;
+  a.W = P.W;
+  a.C = (int)(P.el * P.W);
+  a.mtile_order = P.mtile_order;
+  a.grid_limit = L.ctx->num_sms - FMOE_EP_PUSH_SMS;
+  return a;
+}
+
+// Launch the destination-major push of this rank's send rows on the side
+// stream, ordered after everything issued so far on the layer stream (plan,
+// layouts, pads); ev_pushed marks its end.
+static void ep_push(Layer& L, const void* src, const void* w, int dir) {
+  Ctx* ctx = L.ctx;
+  Layer::Ep& P = *L.ep;
+  if (!P.side) {
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&P.side, cudaStreamNonBlocking, hi));
+    CK(cudaEventCreateWithFlags(&P.ev_go, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&P.ev_pushed, cudaEventDisableTiming));
+  }
+  CK(cudaEventRecord(P.ev_go, ctx->stream));
+  CK(cudaStreamWaitEvent(P.side, P.ev_go, 0));
+  const int64_t E = L.E;
+  CK(cudaMemsetAsync(P.push_ctr, 0, (1 + E) * 4, P.side));
+  const size_t smem = (size_t)(E + 2) * 4;
+  const int base = PH_N * P.W + dir * (int)P.el * P.W;
+  const auto* s16 = static_cast<const __nv_bfloat16*>(src);
+  if (dir == 0)
+    ep_push_kernel<false><<<FMOE_EP_PUSH_SMS, kPushThreads, smem, P.side>>>(
+        s16, L.cfg.d_m, L.plan, nullptr, P.peer.d_ptr[PB_XS], P.g_delta, P.peer.d_ptr[PB_FLAGS], base, P.W, P.r,
+        (int)P.el, P.peer.epoch, P.push_ctr);
+  else
+    ep_push_kernel<true><<<FMOE_EP_PUSH_SMS, kPushThreads, smem, P.side>>>(
+        s16, L.cfg.d_m, L.plan, static_cast<const float*>(w), P.peer.d_ptr[PB_DYS], P.g_delta,
+        P.peer.d_ptr[PB_FLAGS], base, P.W, P.r, (int)P.el, P.peer.epoch, P.push_ctr);
+  CK(cudaGetLastError());
+  ++ctx->launches;
+  CK(cudaEventRecord(P.ev_pushed, P.side));
+}
+
 void Layer::ep_forward(const void* x, void* y) {
   Transport* tr = ep_transport(*this);
   Ep& P = *ep;
@@ -491,17 +702,30 @@ void Layer::ep_forward(const void* x, void* y) {
       ep_plan_peer(*this);                     // C1 + every rank's layout on the host
       zero_pads(ctx, P, rb, P.xs);
     }
+    P.overlap = ep_overlap_ok(*this);
     ctx_mark(ctx, MARK_PLAN);
-    ScatterRoute sr{idx, P.g_rank, P.g_delta, P.peer.d_ptr[PB_XS]};
-    scatter(ctx, t, x, d, plan, nullptr, &sr);  // C2 fused
-    P.peer.signal(ctx, PH_SCATTER);
-    P.peer.wait(ctx, PH_SCATTER);
-    ctx_mark(ctx, MARK_SCATTER);
     const int64_t c = P.el * P.W;
     RowRoute rr{P.peer.d_ptr[PB_YS], P.rt, P.rt + c, P.rt + 2 * c, P.W};
-    experts_fwd(ctx, t, P.rplan, d, h, params(), P.xs, P.hidden, P.ys, relu_bits, nullptr, &rr);  // C3 fused
+    if (P.overlap) {
+      // C2 overlapped with fc1: the rows are pushed by a concurrent kernel on
+      // the side stream (destination-major, per-chunk flags) while fc1, on
+      // the SMs the push leaves free, takes its tiles in arrival order and
+      // starts each as soon as its rows have landed
+      Arrival arr = ep_arrival(*this, 0);
+      ep_push(*this, x, nullptr, 0);
+      ctx_mark(ctx, MARK_SCATTER);
+      experts_fwd(ctx, t, P.rplan, d, h, params(), P.xs, P.hidden, P.ys, relu_bits, nullptr, &rr, &arr);
+    } else {
+      ScatterRoute sr{idx, P.g_rank, P.g_delta, P.peer.d_ptr[PB_XS]};
+      scatter(ctx, t, x, d, plan, nullptr, &sr);  // C2 fused
+      P.peer.signal(ctx, PH_SCATTER);
+      P.peer.wait(ctx, PH_SCATTER);
+      ctx_mark(ctx, MARK_SCATTER);
+      experts_fwd(ctx, t, P.rplan, d, h, params(), P.xs, P.hidden, P.ys, relu_bits, nullptr, &rr);  // C3 fused
+    }
     P.peer.signal(ctx, PH_GATHER);
     P.peer.wait(ctx, PH_GATHER);
+    if (P.overlap) CK(cudaStreamWaitEvent(ctx->stream, P.ev_pushed, 0));  // x read by the push
     gather_combine(ctx, t, ys, d, plan, vals, y);
     ctx_mark(ctx, MARK_GATHER);
     return;
@@ -534,16 +758,30 @@ void Layer::ep_backward(const void* dy, void* dx) {
       ep_zero_pads_device(ctx, P, rb, P.d_ys);
     else
       zero_pads(ctx, P, rb, P.d_ys);
-    ScatterRoute sr{idx, P.g_rank, P.g_delta, P.peer.d_ptr[PB_DYS]};
-    gather_combine_bwd(ctx, t, dy, ys, d, plan, vals, nullptr, d_w, gate ? scores : nullptr,
-                       gate ? idx : nullptr, gate ? dz_bf16 : nullptr, &sr);
-    P.peer.signal(ctx, PH_SCATTER_BWD);
-    P.peer.wait(ctx, PH_SCATTER_BWD);
-    ctx_mark(ctx, MARK_GCB);
     const int64_t c = P.el * P.W;
     RowRoute rr{P.peer.d_ptr[PB_DXS], P.rt, P.rt + c, P.rt + 2 * c, P.W};
-    experts_bwd(ctx, t, P.rplan, d, h, params(), P.xs, P.hidden, P.d_ys, P.d_xs, grads(), P.d_pre, tpart,
-                relu_bits, nullptr, EXPERTS_BWD_DGRAD, &rr);
+    if (P.overlap) {
+      // d_ys = w * d_y pushed by the side stream (destination-major, per-chunk
+      // flags) while gcb computes d_w and the gate Jacobian here and dgrad fc2
+      // consumes the arriving chunks tile by tile
+      ep_push(*this, dy, vals, 1);
+      gather_combine_bwd(ctx, t, dy, ys, d, plan, vals, nullptr, d_w, gate ? scores : nullptr,
+                         gate ? idx : nullptr, gate ? dz_bf16 : nullptr, nullptr);
+      ctx_mark(ctx, MARK_GCB);
+      Arrival arr = ep_arrival(*this, 1);
+      experts_bwd(ctx, t, P.rplan, d, h, params(), P.xs, P.hidden, P.d_ys, P.d_xs, grads(), P.d_pre, tpart,
+                  relu_bits, nullptr, EXPERTS_BWD_DGRAD, &rr, &arr);
+      CK(cudaStreamWaitEvent(ctx->stream, P.ev_pushed, 0));  // dy read by the push
+    } else {
+      ScatterRoute sr{idx, P.g_rank, P.g_delta, P.peer.d_ptr[PB_DYS]};
+      gather_combine_bwd(ctx, t, dy, ys, d, plan, vals, nullptr, d_w, gate ? scores : nullptr,
+                         gate ? idx : nullptr, gate ? dz_bf16 : nullptr, &sr);
+      P.peer.signal(ctx, PH_SCATTER_BWD);
+      P.peer.wait(ctx, PH_SCATTER_BWD);
+      ctx_mark(ctx, MARK_GCB);
+      experts_bwd(ctx, t, P.rplan, d, h, params(), P.xs, P.hidden, P.d_ys, P.d_xs, grads(), P.d_pre, tpart,
+                  relu_bits, nullptr, EXPERTS_BWD_DGRAD, &rr);
+    }
     P.peer.signal(ctx, PH_GATHER_BWD);
     experts_bwd(ctx, t, P.rplan, d, h, params(), P.xs, P.hidden, P.d_ys, P.d_xs, grads(), P.d_pre, tpart,
                 relu_bits, nullptr, EXPERTS_BWD_WGRAD);
@@ -590,6 +828,12 @@ void Layer::ep_backward(const void* dy, void* dx) {
 namespace fmoe_b200 {
 void Layer::ep_free(Ep* e) {
   if (!e) return;
+  if (e->side) {
+    cudaStreamSynchronize(e->side);
+    cudaStreamDestroy(e->side);
+    cudaEventDestroy(e->ev_go);
+    cudaEventDestroy(e->ev_pushed);
+  }
   e->peer.close();
   if (e->h_peer) cudaFreeHost(e->h_peer);
   delete e;

@@ -180,6 +180,17 @@ void gate_bwd(Ctx* ctx, fmoe_dtype t, const void* x, const void* wg, const void*
 }
 
 // ----------------------------------------------------------------- experts
+static void set_arrival(tc::Params& p, const Arrival* a) {
+  if (!a) return;
+  p.arrive_flags = a->flags;
+  p.arrive_epoch = a->epoch;
+  p.arrive_rt = a->rt;
+  p.arrive_W = a->W;
+  p.arrive_C = a->C;
+  p.mtile_order = a->mtile_order;
+  p.grid_limit = a->grid_limit;
+}
+
 static void set_route(tc::Params& p, const RowRoute* r) {
   if (!r) return;
   p.route_out = r->out;
@@ -191,7 +202,7 @@ static void set_route(tc::Params& p, const RowRoute* r) {
 
 void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
                  const fmoe_expert_params& w, const void* xs, void* hidden, void* ys,
-                 uint32_t* relu_bits, void* preact, const RowRoute* ys_route) {
+                 uint32_t* relu_bits, void* preact, const RowRoute* ys_route, const Arrival* arrive) {
   const int64_t E = b.n_experts;
   if (E == 0 || b.capacity == 0) return;
   if (t == FMOE_F64 || t == FMOE_F32) {
@@ -236,6 +247,8 @@ void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     p.epi = tc::EPI_BF16; p.C = hidden; p.ldc = h;
     p.bias = (const float*)w.b1; p.bias_group_stride = h; p.relu = 1;
     p.relu_bits_out = relu_bits;
+    set_arrival(p, arrive);  // EP overlap: tiles wait for their rows, arrival order
+    p.probe = ctx_probe_slot(ctx);
     tc::launch(ctx, 256, false, true, ta, tb, p, max_tiles * ceil_div(h, 256), cg);
     ctx_mark(ctx, MARK_FC1);
   }
@@ -248,6 +261,7 @@ void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     p.epi = tc::EPI_BF16; p.C = ys; p.ldc = d;
     p.bias = (const float*)w.b2; p.bias_group_stride = d; p.relu = 0;
     set_route(p, ys_route);
+    p.probe = ctx_probe_slot(ctx);
     tc::launch(ctx, 256, false, true, ta, tb, p, max_tiles * ceil_div(d, 256), cg);
     ctx_mark(ctx, MARK_FC2);
   }
@@ -256,7 +270,8 @@ void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
 void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
                  const fmoe_expert_params& w, const void* xs, const void* hidden, const void* d_ys,
                  void* d_xs, const fmoe_expert_grads& g, void* d_pre, float* part_ws,
-                 const uint32_t* relu_bits, const void* mask, int phase, const RowRoute* dxs_route) {
+                 const uint32_t* relu_bits, const void* mask, int phase, const RowRoute* dxs_route,
+                 const Arrival* arrive) {
   const int64_t E = b.n_experts;
   if (E == 0) return;
   if (t == FMOE_F64 || t == FMOE_F32) {
@@ -321,7 +336,10 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     p.mode = tc::RAGGED_M; p.M = (int)cap; p.N = (int)h; p.K = (int)d;
     p.tile_group = b.tile_expert; p.n_mtiles = b.n_tiles; p.b_group_rows = (int)h;
     p.epi = tc::EPI_MASK_BF16; p.C = d_pre; p.ldc = h; p.mask = (const __nv_bfloat16*)hidden; p.ldm = h;
+    p.colsum_part = part_ws;  // d_b1 = colsum(d_pre) fused into the epilogue (expert.cpp:51-53)
     p.relu_bits = relu_bits;  // 1 bit per activation instead of re-reading hidden
+    set_arrival(p, arrive);   // EP overlap: tiles wait for their d_ys rows, arrival order
+    p.probe = ctx_probe_slot(ctx);
     tc::launch(ctx, 256, false, false, ta, tb, p, max_tiles * ceil_div(h, 256), cg);
     ctx_mark(ctx, MARK_DGRAD2);
   }
@@ -338,10 +356,16 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     p.mode = tc::RAGGED_K; p.M = (int)h; p.N = (int)d; p.n_groups = (int)E; p.k_offsets = b.offsets;
     p.group_order = group_order;
     p.epi = tc::EPI_F32; p.C = g.d_w2; p.ldc = d; p.c_group_stride = h * d;
-    // d_b2 = colsum(d_ys) per expert (expert.cpp:43-45) from the B tiles this GEMM streams
-    p.bsum_out = (float*)g.d_b2; p.bsum_group_stride = d;
+    p.probe = ctx_probe_slot(ctx);
     tc::launch(ctx, 256, true, true, ta, tb, p, E * ceil_div(h, 128 * cg) * ceil_div(d, 256), cg);
     ctx_mark(ctx, MARK_WGRAD2);
+  }
+  // d_b2 = colsum(d_ys) per expert (expert.cpp:43-45): tile partials + ordered reduce
+  const int64_t t128 = cap / 128;  // 128-row tiles (bias partials)
+  float* part_b2 = part_ws + t128 * h;
+  if (do_wgrad) {
+    tile_colsum(ctx, (const __nv_bfloat16*)d_ys, d, b.n_tiles, t128, part_b2);
+    reduce_tile_partials(ctx, part_b2, d, b.offsets, E, (float*)g.d_b2);
     ctx_mark(ctx, MARK_DB2);
   }
   if (do_dgrad) {  // dgrad fc1: d_xs = d_pre W1^T; B(k=j, n=c) = W1[e][c][j] -> K-major [E*d, h]
@@ -352,6 +376,7 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     p.tile_group = b.tile_expert; p.n_mtiles = b.n_tiles; p.b_group_rows = (int)d;
     p.epi = tc::EPI_BF16; p.C = d_xs; p.ldc = d;
     set_route(p, dxs_route);
+    p.probe = ctx_probe_slot(ctx);
     tc::launch(ctx, 256, false, false, ta, tb, p, max_tiles * ceil_div(d, 256), cg);
     ctx_mark(ctx, MARK_DGRAD1);
   }
@@ -362,10 +387,12 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     p.mode = tc::RAGGED_K; p.M = (int)d; p.N = (int)h; p.n_groups = (int)E; p.k_offsets = b.offsets;
     p.group_order = group_order;
     p.epi = tc::EPI_F32; p.C = g.d_w1; p.ldc = h; p.c_group_stride = d * h;
-    // d_b1 = colsum(d_pre) per expert (expert.cpp:51-53) from the B tiles this GEMM streams
-    p.bsum_out = (float*)g.d_b1; p.bsum_group_stride = h;
+    p.probe = ctx_probe_slot(ctx);
     tc::launch(ctx, 256, true, true, ta, tb, p, E * ceil_div(d, 128 * cg) * ceil_div(h, 256), cg);
     ctx_mark(ctx, MARK_WGRAD1);
+  }
+  if (do_wgrad) {  // d_b1 partials come from the dgrad-fc2 epilogue
+    reduce_tile_partials(ctx, part_ws, h, b.offsets, E, (float*)g.d_b1);
     ctx_mark(ctx, MARK_DB1);
   }
 }

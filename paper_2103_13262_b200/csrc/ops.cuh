@@ -37,9 +37,22 @@ struct RowRoute {
   const int32_t* dst = nullptr;    // [el*W] first row in source s's send layout
   int world = 1;
 };
+// Overlapped expert-parallel exchange (ep.cu): the first GEMM of a pass (fc1
+// forward, dgrad fc2 backward) waits per tile for its rows' chunks to arrive
+// (tc::Params::arrive_*), deals row tiles in `mtile_order` and leaves SMs free
+// for the concurrent push kernel (grid_limit).
+struct Arrival {
+  const uint32_t* flags = nullptr;  // [el*W] chunk flags (local memory, written by the senders)
+  uint32_t epoch = 0;
+  const int32_t* rt = nullptr;      // [start[C], rows[C]]
+  int W = 1, C = 0;
+  const int* mtile_order = nullptr;
+  int grid_limit = 0;
+};
 void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
                  const fmoe_expert_params& w, const void* xs, void* hidden, void* ys,
-                 uint32_t* relu_bits = nullptr, void* preact = nullptr, const RowRoute* ys_route = nullptr);
+                 uint32_t* relu_bits = nullptr, void* preact = nullptr, const RowRoute* ys_route = nullptr,
+                 const Arrival* arrive = nullptr);
 // preact (SIMT dtypes only, optional): also keep x*w1 + b1 before the relu
 // (ForwardCache::preact, expert.hpp:31-35).
 // d_pre_ws: [capacity, h] dtype scratch; mask (SIMT dtypes only, optional): the
@@ -61,7 +74,8 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
                  const fmoe_expert_params& w, const void* xs, const void* hidden, const void* d_ys,
                  void* d_xs, const fmoe_expert_grads& g, void* d_pre_ws, float* part_ws,
                  const uint32_t* relu_bits = nullptr, const void* mask = nullptr,
-                 int phase = EXPERTS_BWD_ALL, const RowRoute* dxs_route = nullptr);
+                 int phase = EXPERTS_BWD_ALL, const RowRoute* dxs_route = nullptr,
+                 const Arrival* arrive = nullptr);
 // allreduce_sum over ctx's transport (ep.cu): in place, ascending-rank order.
 void allreduce_sum(Ctx* c, fmoe_dtype dt, void* buf, int64_t n, const int* group, int64_t gs);
 

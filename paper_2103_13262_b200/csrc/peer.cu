@@ -96,6 +96,9 @@ bool PeerSet::open(Ctx* ctx, int world, int rank, const void* blobs, void** ptr_
   const Blob* all = static_cast<const Blob*>(blobs);
   const Blob& mine = all[r];
   bool good = mine.magic == kMagic;
+  cross_process = true;
+  for (int p = 0; p < W; ++p)
+    if (p != r && all[p].pid == mine.pid) cross_process = false;
   for (int b = 0; b < PB_N; ++b) ptr[b].assign(W, nullptr);
   for (int p = 0; p < W && good; ++p) {
     const Blob& o = all[p];
@@ -202,6 +205,7 @@ void PeerSet::close() {
   for (void* q : opened) cudaIpcCloseMemHandle(q);
   opened.clear();
   lw = nullptr;
+  cross_process = false;
   for (int b = 0; b < PB_N; ++b) {
     d_ptr[b] = nullptr;
     ptr[b].clear();

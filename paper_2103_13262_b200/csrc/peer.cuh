@@ -43,6 +43,10 @@ struct PeerSet {
   void** d_ptr[PB_N] = {};         // device copies of ptr[buf] (W entries, in ptr_table)
   uint32_t epoch = 0;
   LocalWorld* lw = nullptr;        // same-process world: event-ordered phases
+  // every peer lives in another process (one process per GPU, or processes
+  // time-sharing one GPU): kernels may spin on peer-written flags without
+  // starving the kernel that releases them (which the in-process world can)
+  bool cross_process = false;
 
   // Exchange blobs over `tr`; every rank must call it with its local buffers.
   // On any failure every rank falls back together (ok = false everywhere).

@@ -8,6 +8,7 @@
 // order (fma chain for the combine, plain adds for scatter_backward) in the
 // accumulate type (fp64 for FMOE_F64, fp32 otherwise), so FMOE_F64 results
 // are bit-identical to dispatch.cpp.
+#include <algorithm>
 #include <type_traits>
 
 #include "common.cuh"
@@ -482,25 +483,37 @@ __global__ void block_colsum_kernel(const T* __restrict__ src, int64_t n_cols,
 }
 
 // ------------------------------------------------- tile column sums (bf16)
-// part[t][c] = sum of the 128 rows of tile t (fp32).  Two columns per thread,
-// a warp covers 128 contiguous bytes of a row, 128 rows in flight-unrolled order.
-__global__ void tile_colsum_kernel(const __nv_bfloat16* __restrict__ src, int64_t n_cols,
-                                   const int32_t* __restrict__ n_tiles, float* __restrict__ part) {
-  const int64_t t = blockIdx.y;
+// part[t][c] = sum of the 128 rows of tile t (fp32), rows in order.  One block
+// per tile; a thread owns 8 columns (one 16-byte vector per row) and keeps 8
+// rows of loads in flight, so the pass streams d_ys at HBM rate.
+__global__ void __launch_bounds__(256) tile_colsum_kernel(const __nv_bfloat16* __restrict__ src, int64_t n_cols,
+                                                          const int32_t* __restrict__ n_tiles, float* __restrict__ part) {
+  const int64_t t = blockIdx.x;
   if (t >= __ldg(n_tiles)) return;
-  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
-  if (c >= n_cols) return;
-  const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(src + t * 128 * n_cols + c);
-  const int64_t stride = n_cols / 2;
-  float s0 = 0.f, s1 = 0.f;
-#pragma unroll 16
-  for (int r = 0; r < 128; ++r) {
-    const float2 v = __bfloat1622float2(__ldg(p + r * stride));
-    s0 += v.x;
-    s1 += v.y;
+  const int64_t nv = n_cols / 8;
+  for (int64_t v = threadIdx.x; v < nv; v += blockDim.x) {
+    const uint4* p = reinterpret_cast<const uint4*>(src + t * 128 * n_cols) + v;
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+    for (int r = 0; r < 128; r += 8) {
+      uint4 u[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) u[q] = __ldg(p + (r + q) * nv);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t w[4] = {u[q].x, u[q].y, u[q].z, u[q].w};
+#pragma unroll
+        for (int z = 0; z < 4; ++z) {
+          acc[2 * z] += __uint_as_float(w[z] << 16);
+          acc[2 * z + 1] += __uint_as_float(w[z] & 0xffff0000u);
+        }
+      }
+    }
+    float4* o = reinterpret_cast<float4*>(part + t * n_cols + v * 8);
+    o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
   }
-  part[t * n_cols + c] = s0;
-  part[t * n_cols + c + 1] = s1;
 }
 
 // out[e][c] = sum over expert e's tiles, in tile order (deterministic).
@@ -540,8 +553,9 @@ void order_groups_desc(Ctx* ctx, const int32_t* offsets, int64_t groups, int32_t
 void tile_colsum(Ctx* ctx, const __nv_bfloat16* src, int64_t n_cols, const int32_t* n_tiles,
                  int64_t max_tiles, float* part) {
   if (max_tiles == 0 || n_cols == 0) return;
-  dim3 grid((unsigned)ceil_div(n_cols, 512), (unsigned)max_tiles);
-  tile_colsum_kernel<<<grid, 256, 0, ctx->stream>>>(src, n_cols, n_tiles, part);
+  if (n_cols % 8) shape_error("tile_colsum: columns must be a multiple of 8");
+  const int threads = (int)std::min<int64_t>(256, ceil_div(n_cols / 8, 32) * 32);
+  tile_colsum_kernel<<<(unsigned)max_tiles, threads, 0, ctx->stream>>>(src, n_cols, n_tiles, part);
   CK_LAUNCH(ctx);
 }
 

@@ -1,6 +1,7 @@
 // tc_gemm.cu -- see tc_gemm.cuh for the design.
 #include <cuda.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "ptx.cuh"
@@ -17,6 +18,7 @@ struct Cfg {
   static constexpr int B_BYTES = (BN / CG) * BK * 2;   // this CTA's share of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;             // two fp32 accumulators
+  static constexpr int COLSUM_BYTES = EPI == EPI_F32 ? 0 : 4 * BN * 4;  // per-warp column sums of one tile
   // outputs leave through TMA stores from per-warp staging tiles of 32 rows x
   // 64 B (64B swizzle): 32 bf16 columns, or 16 fp32 columns (a 32-column fp32
   // chunk is stored as two halves).  One tile per warp keeps 6 pipeline
@@ -47,12 +49,30 @@ struct Cfg {
 #define FMOE_TC_F32_SMEM_KB FMOE_TC_SMEM_KB
 #endif
   static constexpr int BUDGET =
-      (EPI == EPI_F32 ? FMOE_TC_F32_SMEM_KB : FMOE_TC_SMEM_KB) * 1024 - 1280 /*align + barriers*/ - STORE_BYTES - BIAS_BYTES;
+      (EPI == EPI_F32 ? FMOE_TC_F32_SMEM_KB : FMOE_TC_SMEM_KB) * 1024 - 1280 /*align + barriers*/ - STORE_BYTES - COLSUM_BYTES - BIAS_BYTES;
   static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
   static constexpr int SMEM =
-      STAGES * STAGE_BYTES + STORE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + BIAS_BYTES;
+      STAGES * STAGE_BYTES + STORE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + COLSUM_BYTES + BIAS_BYTES;
   static_assert(SMEM <= 227 * 1024, "tc_gemm: shared memory over the sm_100 per-CTA limit");
 };
+
+// Named barrier among the 4 epilogue warps (ids 1.. are free; 0 = __syncthreads).
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+// After the call lane L holds sum over the warp's 32 lanes of v[L] (31 shuffles).
+__device__ __forceinline__ float warp_transpose_sum(float (&v)[32], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const float send = upper ? v[i] : v[i + o];
+      const float keep = upper ? v[i + o] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return v[0];
+}
 
 // K-major / MN-major canonical SW128 layouts (cute UMMA::make_umma_desc):
 //   K-major : 8-row x 128 B atoms, SBO = 1024 (next 8 rows), LBO unused (=16 B)
@@ -101,8 +121,9 @@ __device__ __forceinline__ Tile decode(const Params& p, int t) {
   Tile r;
   const int nn = n_tiles_n<BN>(p);
   if (p.mode == RAGGED_M) {
-    const int mt = t / nn;
-    r.n0 = (t - mt * nn) * BN;
+    const int mt0 = t / nn;
+    r.n0 = (t - mt0 * nn) * BN;
+    const int mt = p.mtile_order ? __ldg(p.mtile_order + mt0) : mt0;
     r.m0 = mt * BM * CG;
     r.g = p.tile_group ? __ldg(p.tile_group + mt * CG) : 0;
     r.kbeg = 0;
@@ -462,10 +483,11 @@ __device__ __forceinline__ void epi_gate(const Params& p, uint32_t tbase, int ro
 //   BIAS  += bias (staged in shared memory once per tile)
 //   RELU  max(v, 0) and, when p.relu_bits_out, its bitmap (bit = v > 0)
 //   MASK  v * bit of p.relu_bits (relu_backward, strict >)
-template <int BN, int NBUF, bool BIAS, bool RELU, bool MASK>
+//   COLSUM per-column sums of the final values into colsum_smem
+template <int BN, int NBUF, bool BIAS, bool RELU, bool MASK, bool COLSUM>
 __device__ __forceinline__ void drain_bf16(const Params& p, const Tile& tl, const CUtensorMap* tmC, uint32_t tbase,
                                            int c_lo, int row, int out_row, uint32_t stage_base, uint32_t& sbuf,
-                                           const float* bias_s, int lane) {
+                                           const float* bias_s, float* colsum_smem, int q, int lane) {
   constexpr int CPW = BN / 64;
   constexpr uint32_t TILE_BYTES = 32 * 64;
   uint32_t mbits[CPW];
@@ -527,7 +549,33 @@ __device__ __forceinline__ void drain_bf16(const Params& p, const Tile& tl, cons
     __syncwarp();
     tma_store_commit_warp(tmC, stage, tl.n0 + c * 32, out_row);
     sbuf = (sbuf + 1) % NBUF;
+    if constexpr (COLSUM) colsum_smem[q * BN + c * 32 + lane] = warp_transpose_sum(v, lane);
   }
+}
+
+// Overlapped expert-parallel exchange: block until every chunk (expert g,
+// source s) that intersects rows [r0, r0 + BM) has been published by its
+// sender (see Params::arrive_flags).  Lane 0 polls the local flag words with
+// acquire loads; the proxy fence then orders the TMA (async proxy) reads of
+// those rows after the observed release.
+__device__ __forceinline__ void wait_rows_arrived(const Params& p, int g, int r0, int lane) {
+  if (lane == 0) {
+    const int W = p.arrive_W, C = p.arrive_C;
+    for (int s = 0; s < W; ++s) {
+      const int c = g * W + s;
+      const int st = __ldg(p.arrive_rt + c), nr = __ldg(p.arrive_rt + C + c);
+      if (nr <= 0 || st >= r0 + BM || st + nr <= r0) continue;
+      const uint32_t* f = p.arrive_flags + c;
+      while (true) {
+        uint32_t v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if ((int32_t)(v - p.arrive_epoch) >= 0) break;
+        __nanosleep(128);
+      }
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+  __syncwarp();
 }
 
 // ------------------------------------------------------------------ kernel
@@ -553,22 +601,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull = bars + 2 * STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  // B column sums (weight gradients): the MMA warp commits each consumed stage
-  // to mmadone as well; warps 2, 3 read it and release the stage on `empty`
-  constexpr bool BSUM = EPI == EPI_F32 && A_MN && B_MN;
-  uint64_t* mmadone = tempty + 4;  // after the tmem slot (8 bytes)
-  float* bias_smem = reinterpret_cast<float*>(sOut + C::STORE_BYTES + 256);
+  float* colsum_smem = reinterpret_cast<float*>(sOut + C::STORE_BYTES + 256);
+  float* bias_smem = reinterpret_cast<float*>(sOut + C::STORE_BYTES + 256 + C::COLSUM_BYTES);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  if (p.probe && blockIdx.x == 0 && threadIdx.x == 0) {
+    p.probe[0] = clock64();
+    p.probe[1] = globaltimer_ns();
+  }
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(smem_u32(full + s), 1);
-      mbar_init(smem_u32(empty + s), BSUM ? 3 : 1);  // + the two B-sum warps
-      if (BSUM) mbar_init(smem_u32(mmadone + s), 1);
+      mbar_init(smem_u32(empty + s), 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(tfull + a), 1);
@@ -611,6 +659,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (t >= total) continue;
         const Tile tl = decode<BN, CG>(p, t);
         const int brow = (p.mode == RAGGED_M) ? tl.g * p.b_group_rows : tl.kbeg;
+        if (p.arrive_flags && tl.nkb > 0) wait_rows_arrived(p, tl.g, tl.m0 + row_off, lane);
         for (int kb = 0; kb < tl.nkb; ++kb) {
           mbar_wait(smem_u32(empty + stage), phase ^ 1);
           const uint32_t fb = smem_u32(full + stage);
@@ -685,7 +734,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // 4 x K=16 and the commit that frees the stage (in both CTAs of a pair)
             tc_mma_kblock_warp<CG, KA, KB>(d_tmem, (uint32_t)ad, (uint32_t)(da0 >> 32), (uint32_t)bd,
                                            (uint32_t)(db0 >> 32), ID, kb != 0, smem_u32(empty + stage));
-            if constexpr (BSUM) tc_commit_warp<CG>(smem_u32(mmadone + stage));
           } else {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
@@ -702,14 +750,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               tc_commit_pair(smem_u32(empty + stage));
             else
               tc_commit(smem_u32(empty + stage));
-            if constexpr (BSUM) {
-              if (FMOE_TC_MMA_WARP)
-                tc_commit_warp<CG>(smem_u32(mmadone + stage));
-              else if (CG == 2)
-                tc_commit_pair(smem_u32(mmadone + stage));
-              else
-                tc_commit(smem_u32(mmadone + stage));
-            }
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -724,77 +764,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tc_commit(smem_u32(tfull + acc));
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
-      }
-    }
-  } else if (BSUM && (warp == 2 || warp == 3)) {
-    // ==================== B column sums (bias gradients) ====================
-    // Each warp owns half of this CTA's B boxes (64 columns x 64 K rows,
-    // MN-major, 128B swizzle: K row r holds 64 columns in 8 16-byte chunks,
-    // chunk c stored at (c ^ (r & 7))).  Lane = (row offset lane>>3, chunk
-    // lane&7): 16 LDS.128 per box and k-block, 8 fp32 sums per lane, folded
-    // across the 4 row offsets by shuffles at the tile's end: a fixed order.
-    constexpr int NBOX = BN / CG / 64, MY = NBOX / 2 > 0 ? NBOX / 2 : 1;
-    const int box0 = (warp - 2) * MY;
-    const int ro = lane >> 3, c8 = lane & 7;
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int it = 0; it * tstep < total; ++it) {
-      const int t = tile_at(p, it, t0, tstep);
-      if (t >= total) continue;
-      const Tile tl = decode<BN, CG>(p, t);
-      const bool need = p.bsum_out != nullptr && tl.m0 == 0 && box0 < NBOX;
-      float acc[MY][8];
-#pragma unroll
-      for (int b = 0; b < MY; ++b)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[b][i] = 0.f;
-      for (int kb = 0; kb < tl.nkb; ++kb) {
-        mbar_wait(smem_u32(mmadone + stage), phase);
-        if (need) {
-#pragma unroll
-          for (int b = 0; b < MY; ++b) {
-            const uint32_t base = smem_u32(sB + stage * C::B_BYTES) + (uint32_t)(box0 + b) * 8192u;
-#pragma unroll 4
-            for (int r = ro; r < 64; r += 4) {
-              uint32_t w0, w1, w2, w3;
-              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                           : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
-                           : "r"(base + (uint32_t)r * 128u + (((uint32_t)c8 ^ ((uint32_t)r & 7u)) << 4)));
-              const uint32_t w[4] = {w0, w1, w2, w3};
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                acc[b][2 * q] += __uint_as_float(w[q] << 16);
-                acc[b][2 * q + 1] += __uint_as_float(w[q] & 0xffff0000u);
-              }
-            }
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(empty + stage));
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-      if (need) {
-#pragma unroll
-        for (int b = 0; b < MY; ++b)
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            acc[b][i] += __shfl_xor_sync(0xffffffffu, acc[b][i], 8);
-            acc[b][i] += __shfl_xor_sync(0xffffffffu, acc[b][i], 16);
-          }
-        if (ro == 0) {
-#pragma unroll
-          for (int b = 0; b < MY; ++b) {
-            const int col = tl.n0 + n_off + (box0 + b) * 64 + c8 * 8;
-            if (col + 8 <= p.N) {
-              float4* o = reinterpret_cast<float4*>(p.bsum_out + (int64_t)tl.g * p.bsum_group_stride + col);
-              o[0] = make_float4(acc[b][0], acc[b][1], acc[b][2], acc[b][3]);
-              o[1] = make_float4(acc[b][4], acc[b][5], acc[b][6], acc[b][7]);
-            }
-          }
-        }
       }
     }
   } else if (warp >= 4) {
@@ -904,21 +873,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             reinterpret_cast<float4*>(bias_s)[lane] = bb;
             __syncwarp();
             if (p.relu)
-              drain_bf16<BN, C::NBUF, true, true, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
-                                                                sbuf, bias_s, lane);
+              drain_bf16<BN, C::NBUF, true, true, false, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
+                                                                sbuf, bias_s, colsum_smem, q, lane);
             else
-              drain_bf16<BN, C::NBUF, true, false, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
-                                                                 sbuf, bias_s, lane);
+              drain_bf16<BN, C::NBUF, true, false, false, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
+                                                                 sbuf, bias_s, colsum_smem, q, lane);
           } else if (p.relu) {
-            drain_bf16<BN, C::NBUF, false, true, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
-                                                               sbuf, bias_s, lane);
+            drain_bf16<BN, C::NBUF, false, true, false, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
+                                                               sbuf, bias_s, colsum_smem, q, lane);
           } else {
-            drain_bf16<BN, C::NBUF, false, false, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
-                                                                sbuf, bias_s, lane);
+            drain_bf16<BN, C::NBUF, false, false, false, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
+                                                                sbuf, bias_s, colsum_smem, q, lane);
           }
         } else {
-          drain_bf16<BN, C::NBUF, false, false, true>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base, sbuf,
-                                                      bias_s, lane);
+          if (p.colsum_part)
+            drain_bf16<BN, C::NBUF, false, false, true, true>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
+                                                              sbuf, bias_s, colsum_smem, q, lane);
+          else
+            drain_bf16<BN, C::NBUF, false, false, true, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
+                                                               sbuf, bias_s, colsum_smem, q, lane);
+        }
+        if (p.colsum_part) {
+          epi_bar();
+          for (int col = ew * 32 + lane; col < BN; col += 256)
+            p.colsum_part[(int64_t)((tl.m0 + row_off) / BM) * p.N + tl.n0 + col] =
+                colsum_smem[col] + colsum_smem[BN + col] + colsum_smem[2 * BN + col] + colsum_smem[3 * BN + col];
+          epi_bar();
         }
       } else {
         // Software-pipelined drain: the TMEM load of chunk i+1 is in flight
@@ -993,7 +973,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               tma_store_commit_warp(&tmC, stage, tl.n0 + c * 32, out_row);
               sbuf = (sbuf + 1) % C::NBUF;
             }
+            if (p.colsum_part) {  // column sums of the final fp32 values of this tile
+              if (row >= p.M) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = 0.f;
+              }
+              colsum_smem[q * BN + c * 32 + lane] = warp_transpose_sum(v, lane);
+            }
           }
+        }
+        if (p.colsum_part) {
+          epi_bar();
+          for (int col = ew * 32 + lane; col < BN; col += 256)
+            if (tl.n0 + col < p.N)
+              p.colsum_part[(int64_t)((tl.m0 + row_off) / BM) * p.N + tl.n0 + col] =
+                  colsum_smem[col] + colsum_smem[BN + col] + colsum_smem[2 * BN + col] + colsum_smem[3 * BN + col];
+          epi_bar();
         }
       }
       tc_fence_before();
@@ -1016,6 +1011,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     cluster_sync_all();
   else
     __syncthreads();
+  if (p.probe && blockIdx.x == 0 && threadIdx.x == 0) {
+    p.probe[2] = clock64();
+    p.probe[3] = globaltimer_ns();
+  }
   if (warp == 2) {
     tc_fence_after();
     if (CG == 2)
@@ -1097,7 +1096,7 @@ static void launch_t(Ctx* ctx, const CUtensorMap& ta, const CUtensorMap& tb, con
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   });
   // persistent grid: one CTA (CG=1) or CTA pair (CG=2) per tile slot, <= #SMs
-  int64_t grid = ctx->num_sms / CG * CG;
+  int64_t grid = (p.grid_limit > 0 ? std::min<int64_t>(p.grid_limit, ctx->num_sms) : ctx->num_sms) / CG * CG;
   if (max_tiles * CG < grid) grid = max_tiles * CG;
   if (grid < CG) return;
   cudaLaunchConfig_t cfg = {};

@@ -80,19 +80,35 @@ struct Params {
   const __nv_bfloat16* gather_src;  // d_xs [rows][N]
   const int* inverse_pos;           // [M][gk]
   int gk;
+  // optional fused column sums of the epilogue values (RAGGED_M bf16
+  // epilogues): colsum_part[m_tile][N] = sum over the tile's 128 rows, fp32
+  // (bias gradients without re-reading the activation; reduced per expert
+  // by reduce_tile_partials in a fixed order -> deterministic)
+  float* colsum_part;
   // relu bitmaps [rows][N/32]: written by the fc1 epilogue (bit = value > 0),
   // read by the dgrad-fc2 epilogue instead of the bf16 activations (64 MiB
   // instead of 1 GiB at cfg2)
   uint32_t* relu_bits_out;
   const uint32_t* relu_bits;
-  // optional column sums of the B operand over each group's K range
-  // (RAGGED_K weight gradients with an MN-major B: B = d_ys / d_pre, whose
-  // per-expert column sums are the bias gradients d_b2 / d_b1, expert.cpp:
-  // 43-45, 51-53).  Warps 2 and 3 sum the B tiles the MMAs have consumed on
-  // the tiles of M-tile 0 and write bsum_out[g * bsum_group_stride + n] once
-  // per (group, column) in a fixed order: no extra pass over B, no atomics.
-  float* bsum_out;
-  int64_t bsum_group_stride;
+  // Expert parallelism, overlapped exchange (RAGGED_M A operand arriving from
+  // the peers while the GEMM runs): before loading the A rows of a tile the
+  // producer waits until every source rank whose chunk (expert g, source s)
+  // intersects those rows has published it -- arrive_flags[g*W + s] reaches
+  // arrive_epoch (written by the sender with st.release.sys after its rows,
+  // ep_push_kernel) -- so tiles start as their rows land instead of after the
+  // whole exchange.  arrive_rt = [start[el*W], rows[el*W]] of every chunk.
+  const uint32_t* arrive_flags;
+  uint32_t arrive_epoch;
+  const int32_t* arrive_rt;
+  int arrive_W, arrive_C;    // world, chunks (el * W)
+  // RAGGED_M (optional): order in which the (pair) row tiles are dealt --
+  // expected arrival order of their rows under the overlapped exchange
+  const int* mtile_order;
+  // persistent grid cap (0: all SMs); SMs left free run the concurrent push
+  int grid_limit;
+  // optional clock probe (Ctx::d_probe slot): CTA 0 writes (clock64,
+  // globaltimer) at its start and end
+  unsigned long long* probe;
   int tma_out;  // set by launch(): outputs leave through TMA stores
   // Expert parallelism over peer memory (EPI_BF16, RAGGED_M): every output row
   // is stored straight into the rank that sent it (fused global_gather,

@@ -5,6 +5,6 @@ mkdir -p gpurun_out
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 9 -c 9 \
   -o gpurun_out/prof_ours -f python tools/ncu_vs_cublas.py > gpurun_out/ncu_ours.log 2>&1
 echo "ours exit $?" >> gpurun_out/ncu_ours.log
-timeout 1200 ncu --set full --clock-control none -k regex:'nvjet|gemm|xmma|cutlass' -s 3 -c 3 \
+timeout 1200 ncu --set full --clock-control none --nvtx --nvtx-include "cublas/" -c 3 \
   -o gpurun_out/prof_cublas -f python tools/ncu_vs_cublas.py > gpurun_out/ncu_cublas.log 2>&1
 echo "cublas exit $?" >> gpurun_out/ncu_cublas.log
