@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(256, FMOE_GCB_MINB) gcb_kernel(const T* __rest
   const int lane = threadIdx.x & 31;
   const int k = (int)p.k;
   if (i >= p.n_b) {
-    if (p.align <= 1) return;
+    if (p.align <= 1 || d_ys == nullptr) return;
     const int64_t row = pad_row(p, i - p.n_b);
     if (row < 0) return;
     if ((d % V) == 0) {
@@ -292,6 +292,9 @@ __global__ void __launch_bounds__(256, FMOE_GCB_MINB) gcb_kernel(const T* __rest
     return;
   }
   const T* dyr = dy + i * d;
+  // d_ys == NULL without a route: the rows are pushed by ep_push_kernel (the
+  // overlapped exchange); only d_w and the gate Jacobian are produced here
+  const bool write_dys = d_ys != nullptr || route.idx != nullptr;
   float dw_f[8];
   if constexpr (!std::is_same<T, double>::value) {
     if ((d % V) == 0 && k <= 2) {
@@ -356,7 +359,7 @@ __global__ void __launch_bounds__(256, FMOE_GCB_MINB) gcb_kernel(const T* __rest
                 o[e] = wt[j] * g[e];
                 part[j] = fma(g[e], yv[e], part[j]);
               }
-              reinterpret_cast<uint4*>(dr[j])[c0 + 32 * u] = pack16<T, A>(o);
+              if (write_dys) reinterpret_cast<uint4*>(dr[j])[c0 + 32 * u] = pack16<T, A>(o);
             }
           }
         }
@@ -415,15 +418,17 @@ __global__ void __launch_bounds__(256, FMOE_GCB_MINB) gcb_kernel(const T* __rest
             o[u] = wt * g[u];
           part = fma(g[u], yv[u], part);
         }
-        reinterpret_cast<uint4*>(dr)[c] = pack16<T, A>(o);
+        if (write_dys) reinterpret_cast<uint4*>(dr)[c] = pack16<T, A>(o);
       }
     } else {
       for (int64_t c = lane; c < d; c += 32) {
         const A g = (A)to_f(dyr[c]);
-        if constexpr (std::is_same<T, double>::value)
-          dr[c] = __dmul_rn(wt, g);
-        else
-          dr[c] = from_f<T>((float)(wt * g));
+        if (write_dys) {
+          if constexpr (std::is_same<T, double>::value)
+            dr[c] = __dmul_rn(wt, g);
+          else
+            dr[c] = from_f<T>((float)(wt * g));
+        }
         part = fma(g, (A)to_f(yr[c]), part);
       }
     }
