@@ -24,7 +24,7 @@ PROF = os.path.join(ROOT, "profiles")
 STEP_ORDER = ["gate", "plan_hist", "plan_colscan", "plan_offsets", "plan_rank", "scatter", "fc1", "fc2", "gather_combine",
               "gcb", "dgrad_fc2", "dgrad_fc1", "gate_dx", "scatter_bwd", "wgrad_order", "wgrad_fc2", "db2_colsum",
               "db2_reduce",
-              "wgrad_fc1", "db1_reduce", "gate_dwg_offsets", "gate_dwg", "gate_dwg_reduce"]
+              "wgrad_fc1", "db1_reduce", "gate_dwg", "gate_dwg_reduce"]
 
 
 def short(name):
@@ -47,7 +47,12 @@ def launches(tag):
     ids = sorted(per)
     # one step = the launches starting at the first gate GEMM (tc_gemm_kernel<64|128|256, 0, 1, 1, 3>)
     first = next(i for i in ids if "tc_gemm_kernel<" in per[i]["name"] and per[i]["name"].endswith(", 3>"))
-    step = [per[i] for i in ids if i >= first][:len(STEP_ORDER)]
+    # the capture window may start mid-step: rotate so it starts at a gate launch
+    # (consecutive steps launch the same sequence)
+    after = [per[i] for i in ids if i >= first]
+    before = [per[i] for i in ids if i < first]
+    extra = len(ids) - len(STEP_ORDER)  # a window longer than a step repeats its first launches
+    step = (after + (before[extra:] if 0 < extra <= len(before) else before))[:len(STEP_ORDER)]
     total = sum(s["gpu__time_duration.sum"] for s in step)
     lines = [f"# {tag}: kernel launches of one bench step (cfg2, ncu --clock-control none, serialized)", "",
              "Command: `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
