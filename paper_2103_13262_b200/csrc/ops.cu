@@ -5,7 +5,6 @@
 // (tc_gemm.cu): operands are used in their stored layouts through K-major or
 // MN-major TMA descriptors, so no transpose is ever materialised.
 #include <algorithm>
-#include <cstdlib>
 #include <vector>
 
 #include "gemm_simt.cuh"
@@ -50,19 +49,6 @@ void require_bf16_dims(int64_t d, int64_t h) {
 
 // CTA-pair (cta_group::2) tiles need expert blocks aligned to 256 rows.
 int pair_mode(const fmoe_plan& b) { return b.align % 256 == 0 ? 2 : 1; }
-
-// Tile width of expert GEMM `which` (bit of FMOE_TC_WIDE, default: fc2, dgrad
-// fc1 and both weight gradients): 512-column pair tiles need CTA pairs and
-// N % 512 == 0; the short-K GEMMs (fc1, dgrad fc2: K = d_m) keep 256 so their
-// epilogue overlaps the next tile's MMAs through two accumulators.
-enum WideBit : int { W_FC1 = 1, W_FC2 = 2, W_DGRAD2 = 4, W_DGRAD1 = 8, W_WGRAD2 = 16, W_WGRAD1 = 32 };
-int expert_bn(int which, int cg, int64_t n) {
-  static const int mask = [] {
-    const char* e = std::getenv("FMOE_TC_WIDE");
-    return e ? std::atoi(e) : (W_FC2 | W_DGRAD1 | W_WGRAD2 | W_WGRAD1);
-  }();
-  return (cg == 2 && n % 512 == 0 && (mask & which)) ? 512 : 256;
-}
 
 std::vector<int32_t> host_counts(Ctx* ctx, const fmoe_plan& b) {
   std::vector<int32_t> c((size_t)b.n_experts);
@@ -263,8 +249,7 @@ void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     p.relu_bits_out = relu_bits;
     set_arrival(p, arrive);  // EP overlap: tiles wait for their rows, arrival order
     p.probe = ctx_probe_slot(ctx);
-    const int bn = expert_bn(W_FC1, cg, h);
-    tc::launch(ctx, bn, false, true, ta, tb, p, max_tiles * ceil_div(h, bn), cg);
+    tc::launch(ctx, 256, false, true, ta, tb, p, max_tiles * ceil_div(h, 256), cg);
     ctx_mark(ctx, MARK_FC1);
   }
   {  // fc2: A = hidden [cap, h] K-major; B = W2 [E*h, d] MN-major
@@ -277,8 +262,7 @@ void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     p.bias = (const float*)w.b2; p.bias_group_stride = d; p.relu = 0;
     set_route(p, ys_route);
     p.probe = ctx_probe_slot(ctx);
-    const int bn = expert_bn(W_FC2, cg, d);
-    tc::launch(ctx, bn, false, true, ta, tb, p, max_tiles * ceil_div(d, bn), cg);
+    tc::launch(ctx, 256, false, true, ta, tb, p, max_tiles * ceil_div(d, 256), cg);
     ctx_mark(ctx, MARK_FC2);
   }
 }
@@ -356,8 +340,7 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     p.relu_bits = relu_bits;  // 1 bit per activation instead of re-reading hidden
     set_arrival(p, arrive);   // EP overlap: tiles wait for their d_ys rows, arrival order
     p.probe = ctx_probe_slot(ctx);
-    const int bn = expert_bn(W_DGRAD2, cg, h);
-    tc::launch(ctx, bn, false, false, ta, tb, p, max_tiles * ceil_div(h, bn), cg);
+    tc::launch(ctx, 256, false, false, ta, tb, p, max_tiles * ceil_div(h, 256), cg);
     ctx_mark(ctx, MARK_DGRAD2);
   }
   // weight-gradient tiles heaviest expert first (skewed routing)
@@ -374,8 +357,7 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     p.group_order = group_order;
     p.epi = tc::EPI_F32; p.C = g.d_w2; p.ldc = d; p.c_group_stride = h * d;
     p.probe = ctx_probe_slot(ctx);
-    const int bn = expert_bn(W_WGRAD2, cg, d);
-    tc::launch(ctx, bn, true, true, ta, tb, p, E * ceil_div(h, 128 * cg) * ceil_div(d, bn), cg);
+    tc::launch(ctx, 256, true, true, ta, tb, p, E * ceil_div(h, 128 * cg) * ceil_div(d, 256), cg);
     ctx_mark(ctx, MARK_WGRAD2);
   }
   // d_b2 = colsum(d_ys) per expert (expert.cpp:43-45): tile partials + ordered reduce
@@ -395,8 +377,7 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     p.epi = tc::EPI_BF16; p.C = d_xs; p.ldc = d;
     set_route(p, dxs_route);
     p.probe = ctx_probe_slot(ctx);
-    const int bn = expert_bn(W_DGRAD1, cg, d);
-    tc::launch(ctx, bn, false, false, ta, tb, p, max_tiles * ceil_div(d, bn), cg);
+    tc::launch(ctx, 256, false, false, ta, tb, p, max_tiles * ceil_div(d, 256), cg);
     ctx_mark(ctx, MARK_DGRAD1);
   }
   if (do_wgrad) {  // wgrad fc1: d_w1[e] = xs_e^T d_pre_e  (M = d, N = h)
@@ -407,8 +388,7 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     p.group_order = group_order;
     p.epi = tc::EPI_F32; p.C = g.d_w1; p.ldc = h; p.c_group_stride = d * h;
     p.probe = ctx_probe_slot(ctx);
-    const int bn = expert_bn(W_WGRAD1, cg, h);
-    tc::launch(ctx, bn, true, true, ta, tb, p, E * ceil_div(d, 128 * cg) * ceil_div(h, bn), cg);
+    tc::launch(ctx, 256, true, true, ta, tb, p, E * ceil_div(d, 128 * cg) * ceil_div(h, 256), cg);
     ctx_mark(ctx, MARK_WGRAD1);
   }
   if (do_wgrad) {  // d_b1 partials come from the dgrad-fc2 epilogue

@@ -223,7 +223,7 @@ __device__ __forceinline__ void tma_load_2d_warp(uint32_t dst, const CUtensorMap
 }
 // One k-block (4 x K=16) and its commit under a single elect: descriptors
 // a_lo + i*KA / b_lo + i*KB, high words constant.
-template <int CG, uint32_t KA, uint32_t KB, bool COMMIT = true>
+template <int CG, uint32_t KA, uint32_t KB>
 __device__ __forceinline__ void tc_mma_kblock_warp(uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo,
                                                    uint32_t b_hi, uint32_t idesc, uint32_t accumulate,
                                                    uint32_t bar) {
@@ -242,17 +242,7 @@ __device__ __forceinline__ void tc_mma_kblock_warp(uint32_t d_tmem, uint32_t a_l
   "@e tcgen05.mma.cta_group::" GRP ".kind::f16 [%0], a1, b1, %5, 1;\n\t"                  \
   "@e tcgen05.mma.cta_group::" GRP ".kind::f16 [%0], a2, b2, %5, 1;\n\t"                  \
   "@e tcgen05.mma.cta_group::" GRP ".kind::f16 [%0], a3, b3, %5, 1;\n\t" COMMIT "}"
-  if constexpr (!COMMIT && CG == 2)
-    asm volatile(FMOE_KB_BODY("2", "")
-                 ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate), "r"(bar),
-                 "n"(KA), "n"(2 * KA), "n"(3 * KA), "n"(KB), "n"(2 * KB), "n"(3 * KB)
-                 : "memory");
-  else if constexpr (!COMMIT)
-    asm volatile(FMOE_KB_BODY("1", "")
-                 ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate), "r"(bar),
-                 "n"(KA), "n"(2 * KA), "n"(3 * KA), "n"(KB), "n"(2 * KB), "n"(3 * KB)
-                 : "memory");
-  else if constexpr (CG == 2)
+  if constexpr (CG == 2)
     asm volatile(FMOE_KB_BODY("2", "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
                                     "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster"
                                     ".multicast::cluster.b64 [%7], m;\n\t}\n\t")

@@ -14,19 +14,11 @@ namespace tc {
 // per CTA pair, each CTA holding its 128 rows of A and BN/2 rows of B.
 template <int BN, int CG = 1, int EPI = EPI_F32>
 struct Cfg {
-  // BN = 512 ("wide"): a 256 x 512 pair tile (128 x 512 per CTA) issued as two
-  // N = 256 MMAs per K step into one 512-column accumulator (all of TMEM).
-  // 171 FLOP per L2 byte instead of 128 for 256 x 256 -- the tile cuBLAS's
-  // nvjet kernels use (profiles/r02c_cublas_nvjet.csv); the epilogue drains
-  // the two halves in order so the next tile's first half starts early.
-  static constexpr bool WIDE = BN == 512;
-  static constexpr int NH = WIDE ? 2 : 1;              // MMA halves (N <= 256 each)
-  static constexpr int HW = BN / NH;                   // columns per half
   static constexpr int A_BYTES = BM * BK * 2;          // 16 KiB: this CTA's 128 rows
   static constexpr int B_BYTES = (BN / CG) * BK * 2;   // this CTA's share of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int TMEM_COLS = WIDE ? 512 : 2 * BN;  // one 512-col / two fp32 accumulators
-  static constexpr int COLSUM_BYTES = (EPI == EPI_F32 || WIDE) ? 0 : 4 * BN * 4;  // per-warp column sums of one tile
+  static constexpr int TMEM_COLS = 2 * BN;             // two fp32 accumulators
+  static constexpr int COLSUM_BYTES = EPI == EPI_F32 ? 0 : 4 * BN * 4;  // per-warp column sums of one tile
   // outputs leave through TMA stores from per-warp staging tiles of 32 rows x
   // 64 B (64B swizzle): 32 bf16 columns, or 16 fp32 columns (a 32-column fp32
   // chunk is stored as two halves).  One tile per warp keeps 6 pipeline
@@ -57,8 +49,7 @@ struct Cfg {
 #define FMOE_TC_F32_SMEM_KB FMOE_TC_SMEM_KB
 #endif
   static constexpr int BUDGET =
-      (WIDE ? 227 : EPI == EPI_F32 ? FMOE_TC_F32_SMEM_KB : FMOE_TC_SMEM_KB) * 1024 - 1280 /*align + barriers*/ -
-      STORE_BYTES - COLSUM_BYTES - BIAS_BYTES;
+      (EPI == EPI_F32 ? FMOE_TC_F32_SMEM_KB : FMOE_TC_SMEM_KB) * 1024 - 1280 /*align + barriers*/ - STORE_BYTES - COLSUM_BYTES - BIAS_BYTES;
   static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
   static constexpr int SMEM =
       STAGES * STAGE_BYTES + STORE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + COLSUM_BYTES + BIAS_BYTES;
@@ -97,8 +88,7 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, bool mn) {
   return d;
 }
 
-// Instruction descriptor, kind::f16: D f32, A/B bf16, M=128*CG, N=BN (<= 256:
-// the wide tile issues two of them).
+// Instruction descriptor, kind::f16: D f32, A/B bf16, M=128*CG, N=BN.
 template <int BN, bool A_MN, bool B_MN, int CG>
 __device__ __forceinline__ constexpr uint32_t idesc() {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) | ((B_MN ? 1u : 0u) << 16) |
@@ -494,10 +484,11 @@ __device__ __forceinline__ void epi_gate(const Params& p, uint32_t tbase, int ro
 //   RELU  max(v, 0) and, when p.relu_bits_out, its bitmap (bit = v > 0)
 //   MASK  v * bit of p.relu_bits (relu_backward, strict >)
 //   COLSUM per-column sums of the final values into colsum_smem
-template <int BN, int CPW, int NBUF, bool BIAS, bool RELU, bool MASK, bool COLSUM>
+template <int BN, int NBUF, bool BIAS, bool RELU, bool MASK, bool COLSUM>
 __device__ __forceinline__ void drain_bf16(const Params& p, const Tile& tl, const CUtensorMap* tmC, uint32_t tbase,
                                            int c_lo, int row, int out_row, uint32_t stage_base, uint32_t& sbuf,
                                            const float* bias_s, float* colsum_smem, int q, int lane) {
+  constexpr int CPW = BN / 64;
   constexpr uint32_t TILE_BYTES = 32 * 64;
   uint32_t mbits[CPW];
   if constexpr (MASK) {
@@ -653,6 +644,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
   const int total = total_tiles<BN, CG>(p);
   const int row_off = (int)rank * BM;             // this CTA's rows inside a pair tile
+  const int n_off = (int)rank * (BN / CG);        // this CTA's B rows (N) inside the tile
 
   if (warp == 0) {
 #ifndef FMOE_TC_TMA_WARP
@@ -694,17 +686,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int j = 0; j < BM / 64; ++j)
               load(a_dst + j * 8192, &tmA, tl.m0 + row_off + 64 * j, tl.kbeg + kb * BK);
           }
-          // B: per MMA half hh, this CTA's HW/CG columns n0 + hh*HW + rank*HW/CG
+          if (!B_MN) {
+            load(b_dst, &tmB, kb * BK, brow + tl.n0 + n_off);
+          } else {
 #pragma unroll
-          for (int hh = 0; hh < C::NH; ++hh) {
-            const int ncol = tl.n0 + hh * C::HW + (int)rank * (C::HW / CG);
-            const uint32_t bd = b_dst + hh * (C::B_BYTES / C::NH);
-            if (!B_MN) {
-              load(bd, &tmB, kb * BK, brow + ncol);
-            } else {
-#pragma unroll
-              for (int j = 0; j < C::HW / CG / 64; ++j) load(bd + j * 8192, &tmB, ncol + 64 * j, brow + kb * BK);
-            }
+            for (int j = 0; j < BN / CG / 64; ++j)
+              load(b_dst + j * 8192, &tmB, tl.n0 + n_off + 64 * j, brow + kb * BK);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -719,7 +706,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #endif
     if (rank == 0 && (FMOE_TC_MMA_WARP || lane == 0)) {
       // ======================= MMA issuer =========================
-      constexpr uint32_t ID = idesc<C::HW, A_MN, B_MN, CG>();
+      constexpr uint32_t ID = idesc<BN, A_MN, B_MN, CG>();
       // descriptors: constant fields + the 16-byte start address (bits 0..13;
       // stage bases are 1 KiB aligned and below 228 KiB, so adding the k
       // offsets never carries out of the field)
@@ -734,37 +721,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (t >= total) continue;
         const Tile tl = decode<BN, CG>(p, t);
         if (tl.nkb == 0) continue;
-        if constexpr (C::WIDE) {
-          // one 512-column accumulator: half hh of the first K step waits for
-          // the epilogue to have drained half hh of the previous tile
-          for (int kb = 0; kb < tl.nkb; ++kb) {
-            mbar_wait(smem_u32(full + stage), phase);
-            tc_fence_after();
-            const uint64_t ad = da0 + (uint64_t)(stage * (C::A_BYTES / 16));
-            const uint64_t bd = db0 + (uint64_t)(stage * (C::B_BYTES / 16));
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-              if (kb == 0) {
-                mbar_wait(smem_u32(tempty + hh), acc_phase ^ 1);
-                tc_fence_after();
-              }
-              const uint32_t bh = (uint32_t)bd + (uint32_t)(hh * (C::B_BYTES / 2 / 16));
-              if (hh == 0)
-                tc_mma_kblock_warp<CG, KA, KB, false>(tmem_base, (uint32_t)ad, (uint32_t)(da0 >> 32), bh,
-                                                      (uint32_t)(db0 >> 32), ID, kb != 0, 0u);
-              else
-                tc_mma_kblock_warp<CG, KA, KB, true>(tmem_base + 256, (uint32_t)ad, (uint32_t)(da0 >> 32), bh,
-                                                     (uint32_t)(db0 >> 32), ID, kb != 0, smem_u32(empty + stage));
-            }
-            if (++stage == STAGES) {
-              stage = 0;
-              phase ^= 1;
-            }
-          }
-          tc_commit_warp<CG>(smem_u32(tfull));
-          acc_phase ^= 1;
-          continue;
-        }
         mbar_wait(smem_u32(tempty + acc), acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -776,7 +732,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if constexpr (FMOE_TC_MMA_WARP == 3) {
             static_assert(BK / 16 == 4, "k-block issue form assumes BK = 64");
             // 4 x K=16 and the commit that frees the stage (in both CTAs of a pair)
-            tc_mma_kblock_warp<CG, KA, KB, true>(d_tmem, (uint32_t)ad, (uint32_t)(da0 >> 32), (uint32_t)bd,
+            tc_mma_kblock_warp<CG, KA, KB>(d_tmem, (uint32_t)ad, (uint32_t)(da0 >> 32), (uint32_t)bd,
                                            (uint32_t)(db0 >> 32), ID, kb != 0, smem_u32(empty + stage));
           } else {
 #pragma unroll
@@ -817,7 +773,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int q = warp & 3;
     const int ew = warp - 4;  // 0..7
     constexpr int NC = BN / 32;
-    constexpr int CPW_T = NC / (2 * C::NH);  // chunks per warp (per half of a wide tile)
+    const int c_lo = (ew >> 2) * (NC / 2), c_hi = c_lo + NC / 2;
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t sbuf = 0;  // TMA-store staging tile in use (per warp, double-buffered)
@@ -829,8 +785,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (tl.nkb == 0) {
         // empty K range (expert without tokens): gradient is exactly zero
         if constexpr (EPI == EPI_F32) {
-          for (int cc = 0; cc < C::NH * CPW_T; ++cc) {
-            const int c = (cc / CPW_T) * (NC / C::NH) + (ew >> 2) * CPW_T + cc % CPW_T;
+          for (int c = c_lo; c < c_hi; ++c) {
             float z[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) z[i] = 0.f;
@@ -860,9 +815,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       mbar_wait(smem_u32(tfull + acc), acc_phase);
       tc_fence_after();
-      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (C::WIDE ? 0 : acc * BN);
-      for (int hh = 0; hh < C::NH; ++hh) {  // wide tiles: half 0, release it, then half 1
-      const int c_lo = hh * (NC / C::NH) + (ew >> 2) * CPW_T, c_hi = c_lo + CPW_T;
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       if constexpr (EPI == EPI_GATE) {
       } else if (EPI == EPI_GATE_DX && p.gk <= 2) {
         // scatter_backward gather fused with the gate d_x: the row's k source
@@ -914,31 +867,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int out_row = tl.m0 + row_off + q * 32;
         float* bias_s = bias_smem + ew * (BN / 2);
         if constexpr (EPI == EPI_BF16) {
-          if (p.bias) {  // this warp's 128 bias columns -> shared memory, once per tile (half)
-            __syncwarp();
+          if (p.bias) {  // this warp's 128 bias columns -> shared memory, once per tile
             const float4 bb = __ldg(reinterpret_cast<const float4*>(p.bias + (int64_t)tl.g * p.bias_group_stride +
                                                                    tl.n0 + c_lo * 32) + lane);
             reinterpret_cast<float4*>(bias_s)[lane] = bb;
             __syncwarp();
             if (p.relu)
-              drain_bf16<BN, CPW_T, C::NBUF, true, true, false, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
+              drain_bf16<BN, C::NBUF, true, true, false, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
                                                                 sbuf, bias_s, colsum_smem, q, lane);
             else
-              drain_bf16<BN, CPW_T, C::NBUF, true, false, false, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
+              drain_bf16<BN, C::NBUF, true, false, false, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
                                                                  sbuf, bias_s, colsum_smem, q, lane);
           } else if (p.relu) {
-            drain_bf16<BN, CPW_T, C::NBUF, false, true, false, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
+            drain_bf16<BN, C::NBUF, false, true, false, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
                                                                sbuf, bias_s, colsum_smem, q, lane);
           } else {
-            drain_bf16<BN, CPW_T, C::NBUF, false, false, false, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
+            drain_bf16<BN, C::NBUF, false, false, false, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
                                                                 sbuf, bias_s, colsum_smem, q, lane);
           }
         } else {
           if (p.colsum_part)
-            drain_bf16<BN, CPW_T, C::NBUF, false, false, true, true>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
+            drain_bf16<BN, C::NBUF, false, false, true, true>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
                                                               sbuf, bias_s, colsum_smem, q, lane);
           else
-            drain_bf16<BN, CPW_T, C::NBUF, false, false, true, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
+            drain_bf16<BN, C::NBUF, false, false, true, false>(p, tl, &tmC, tbase, c_lo, row, out_row, stage_base,
                                                                sbuf, bias_s, colsum_smem, q, lane);
         }
         if (p.colsum_part) {
@@ -952,7 +904,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // Software-pipelined drain: the TMEM load of chunk i+1 is in flight
         // while chunk i is transformed and stored; relu bitmaps are fetched
         // up front.
-        constexpr int CPW = CPW_T;
+        constexpr int CPW = NC / 2;
         uint32_t mbits[CPW];
 #pragma unroll
         for (int i = 0; i < CPW; ++i) {
@@ -1041,20 +993,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      const int rel = C::WIDE ? hh : acc;  // accumulator (half) this warp is done with
       if (lane == 0) {  // the leader's MMA waits for both CTAs' epilogues
         if (rank == 0)
-          mbar_arrive(smem_u32(tempty + rel));
+          mbar_arrive(smem_u32(tempty + acc));
         else
-          mbar_arrive_cluster(mapa_shared(smem_u32(tempty + rel), 0));
+          mbar_arrive_cluster(mapa_shared(smem_u32(tempty + acc), 0));
       }
-      }  // halves
-      if (C::WIDE) {
-        acc_phase ^= 1;
-      } else {
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
-      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
     }
     if constexpr (C::TMA_STORE) {
       if (lane == 0) bulk_wait_all();  // outputs written before the CTA retires
@@ -1183,10 +1129,6 @@ void launch(Ctx* ctx, int bn, bool a_mn, bool b_mn, const CUtensorMap& ta, const
   FMOE_TC_CASE(256, false, false, 2, EPI_MASK_BF16)  // dgrad fc2 (+relu mask, d_b1 column sums)
   FMOE_TC_CASE(256, false, false, 2, EPI_BF16)       // dgrad fc1
   FMOE_TC_CASE(256, true, true, 2, EPI_F32)          // weight gradients
-  // wide 256 x 512 pair tiles (long-K expert GEMMs, N % 512 == 0)
-  FMOE_TC_CASE(512, false, true, 2, EPI_BF16)        // fc2 (fc1)
-  FMOE_TC_CASE(512, false, false, 2, EPI_BF16)       // dgrad fc1
-  FMOE_TC_CASE(512, true, true, 2, EPI_F32)          // weight gradients
   // expert pool, single CTAs (128-row aligned plans)
   FMOE_TC_CASE(256, false, true, 1, EPI_BF16)
   FMOE_TC_CASE(256, false, false, 1, EPI_MASK_BF16)

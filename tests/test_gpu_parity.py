@@ -492,46 +492,3 @@ def test_layer_f32_vs_oracle(fm, orc):
     for a, key in ((layer.d_wg, "dwg"), (layer.grads.d_w1, "dw1"), (layer.grads.d_b1, "db1"),
                    (layer.grads.d_w2, "dw2"), (layer.grads.d_b2, "db2")):
         assert rel_l2(host(a), o[key]) <= 1e-4, key
-
-
-_WIDE_SCRIPT = r"""
-import sys, torch
-sys.path.insert(0, sys.argv[1])
-import paper_2103_13262_b200 as fm
-n, d, h, e, k = 16384, 512, 1024, 8, 2
-torch.cuda.set_device(0)
-layer = fm.MoELayer(fm.MoEConfig(n, d, h, k, e, 1, 5), dtype=torch.bfloat16)
-g = torch.Generator(device="cuda").manual_seed(3)
-x = (torch.rand(n, d, device="cuda", generator=g) * 2 - 1).bfloat16()
-dy = (torch.rand(n, d, device="cuda", generator=g) * 2 - 1).bfloat16()
-y = layer.forward(x)
-dx = layer.backward(dy)
-torch.cuda.synchronize()
-torch.save({"y": y.cpu(), "dx": dx.cpu(), "dw1": layer.grads.d_w1.cpu(), "dw2": layer.grads.d_w2.cpu(),
-            "db1": layer.grads.d_b1.cpu(), "db2": layer.grads.d_b2.cpu(), "dwg": layer.d_wg.cpu()}, sys.argv[2])
-"""
-
-
-@pytest.mark.parametrize("mask", ["0", "63"])
-def test_wide_tiles_equal_narrow_bitwise(tmp_path, mask):
-    """The 256 x 512 pair tiles (two N = 256 MMAs per K step into one
-    512-column accumulator) compute every output element with the same K-step
-    sequence as the 256 x 256 tiles: y, d_x and every gradient are
-    bit-identical whichever GEMMs run wide (FMOE_TC_WIDE bit mask; default =
-    fc2, dgrad fc1 and the weight gradients; 63 = all six; 0 = none)."""
-    import os
-    import subprocess
-    import sys
-
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    outs = {}
-    for m in ("default", mask):
-        env = dict(os.environ)
-        env.pop("FMOE_TC_WIDE", None)
-        if m != "default":
-            env["FMOE_TC_WIDE"] = m
-        path = str(tmp_path / f"out_{m}.pt")
-        subprocess.run([sys.executable, "-c", _WIDE_SCRIPT, root, path], check=True, env=env, timeout=300)
-        outs[m] = torch.load(path)
-    for key in outs["default"]:
-        assert torch.equal(outs["default"][key], outs[mask][key]), key
