@@ -39,12 +39,17 @@ METRIC = "MoE-layer fwd+bwd tokens/s at 1/2/4/8 B200; expert-GEMM % of tensor pe
 UNIT = "tokens/s"
 CFG2 = dict(n_b=65536, d_m=1024, d_h=4096, n_e_local=64, k=2)          # 1 GPU
 CFG3 = dict(n_b=16384, d_m=2048, d_h=8192, n_e_local=8, k=2)           # EP, per GPU
+CFG1 = dict(n_b=8192, d_m=1024, d_h=4096, n_e_local=16, k=2)           # fp32, the reference CPU path's config
 CFG4_LAYERS = 12
 ZIPF_S = 1.0
 
 
 def workload_cfg(name: str, world: int) -> dict:
     """Per-GPU shape of a BASELINE workload at `world` GPUs."""
+    if name == "cfg1":  # BASELINE configs[0]: the reference's own fp32 config, one GPU
+        if world != 1:
+            raise SystemExit("cfg1 is the single-GPU fp32 config (BASELINE configs[0])")
+        return dict(CFG1)
     if name == "cfg2":  # the cfg2 layer (64 experts in total), 65536 tokens per GPU, sharded over the world
         if CFG2["n_e_local"] % world:
             raise SystemExit("cfg2 needs the world size to divide its 64 experts")
@@ -183,7 +188,8 @@ def cpu_reference(n_tokens: int, cfg: dict, min_seconds: float = 10.0, max_reps:
     if not bindings.ref_available():
         return None
     e_total = e_total or cfg["n_e_local"]
-    lib = C.CDLL(bindings.REF_SO)
+    so, build = bindings.ref_timing_so()
+    lib = C.CDLL(so)
     routed = workload == "cfg5"
     if routed:
         import numpy as np
@@ -220,11 +226,14 @@ def cpu_reference(n_tokens: int, cfg: dict, min_seconds: float = 10.0, max_reps:
     what = ("Zipf-routed dispatch + expert pool (build_plan .. scatter_backward)" if routed
             else "forward+backward")
     stack = f", rate / {n_layers} layers" if n_layers > 1 else ""
+    full = n_tokens >= cfg["n_b"]
     return {"value": n_tokens / mean / n_layers, "unit": UNIT, "cores": cores, "kind": "reference",
+            "reps": len(times), "tokens_per_rep": n_tokens, "s_per_rep": mean, "build": build,
             "sample": (f"{n_tokens} tokens of d_m={cfg['d_m']} d_h={cfg['d_h']} E={e_total} "
-                       f"k={cfg['k']} (the GPU workload's layer, token-subsampled), fp64, reference "
+                       f"k={cfg['k']} (" + ("the full workload" if full else "the GPU workload's layer, "
+                                            "token-subsampled") + f"), fp64, reference "
                        f"{what}{stack}, warm-up 1 + {len(times)} reps, mean {mean:.2f} s/step, "
-                       f"FMOE_THREADS={cores}")}
+                       f"FMOE_THREADS={cores}, built {build}")}
 
 
 def cpu_tokens_for(cores: int) -> int:
@@ -238,8 +247,9 @@ def main():
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="default", choices=["default", "cfg2", "cfg3", "cfg4", "cfg5"],
-                    help="BASELINE config (SURVEY §8d); default cfg2: its layer at every N (weak scaling)")
+    ap.add_argument("--workload", default="default", choices=["default", "cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
+                    help="BASELINE config (SURVEY §8d); default cfg2: its layer at every N (weak scaling); "
+                         "cfg1: the reference's fp32 config (8192 tokens, 16 experts) through FMOE_F32")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--graph", action="store_true",
@@ -263,6 +273,8 @@ def n_layers_of(workload: str) -> int:
 
 
 def cpu_sample_tokens(workload: str, cores: int) -> int:
+    if workload == "cfg1":  # the reference's own config: full size (warm-up 1 + 3 reps)
+        return CFG1["n_b"]
     n = cpu_tokens_for(cores)
     return max(256, n // 4) if workload == "cfg4" else n
 
@@ -272,15 +284,19 @@ def run_reference(args, world, rank, cfg):
         return 0
     cores = os.cpu_count() or 1
     n_tok = cpu_sample_tokens(args.workload, cores)
-    res = cpu_reference(n_tok, cfg, min_seconds=max(10.0, 2.0 * args.steps),
-                        max_reps=max(2, min(args.steps, 10)), workload=args.workload,
-                        n_layers=n_layers_of(args.workload), e_total=cfg["n_e_local"] * world)
+    reps = 3 if args.workload == "cfg1" else max(2, min(args.steps, 10))
+    res = cpu_reference(n_tok, cfg, min_seconds=max(10.0, 2.0 * args.steps), max_reps=reps,
+                        workload=args.workload, n_layers=n_layers_of(args.workload),
+                        e_total=cfg["n_e_local"] * world)
     if res is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libfmoe_ref.so not built"}))
         return 0
+    # a step of this arm = one timed rep of the (sampled) workload: steps and
+    # ms_per_step are what actually ran, so steps x ms_per_step fits the run
     line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "ms_per_step": 1e3 * cfg["n_b"] * world / res["value"], "dtype": "f64", "data": "synthetic",
+            "steps": res["reps"], "steps_requested": args.steps, "warmup": 1, "higher_is_better": True,
+            "ms_per_step": 1e3 * res["s_per_rep"], "tokens_per_step": res["tokens_per_rep"],
+            "ms_per_full_workload_step": 1e3 * cfg["n_b"] * world / res["value"], "dtype": "f64", "data": "synthetic",
             "scaling": "weak", "vs_baseline": None,
             "config": {"workload": workload_name(args.workload, cfg, world), **cfg, "world": world},
             "cpu_baseline": res,
@@ -290,6 +306,10 @@ def run_reference(args, world, rank, cfg):
 
 
 def workload_name(workload, cfg, world):
+    if workload == "cfg1":
+        return ("cfg1: single MoE layer d_model=1024 d_hidden=4096, 16 experts top-2, 8192 tokens, fp32 "
+                "(FMOE_F32: gate and permutes in fp32, expert GEMMs as bf16x3 split products on the tensor "
+                "cores, fp32 accumulate), fwd+bwd")
     if workload == "cfg2":
         if world == 1:
             return ("cfg2: single MoE layer d_model=1024 d_hidden=4096, 64 experts top-2, 65536 tokens, "
@@ -340,19 +360,21 @@ def run_ours(args, world, rank, cfg):
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         mcfg = fm.MoEConfig(n, d, h, k, el, world, SEED)
+        dt = torch.float32 if wl == "cfg1" else torch.bfloat16
         if wl == "cfg4":
-            model = MoEStack(mcfg, n_layers, rank=rank, dtype=torch.bfloat16)
+            model = MoEStack(mcfg, n_layers, rank=rank, dtype=dt)
             layer0 = model.layers[0]
         else:
-            model = layer0 = fm.MoELayer(mcfg, rank=rank, dtype=torch.bfloat16)
+            model = layer0 = fm.MoELayer(mcfg, rank=rank, dtype=dt)
         if shared:
             model.connect_peers(dist)
         elif world > 1:
             model.connect(dist)
         g = torch.Generator(device="cuda")
         g.manual_seed(1000 + rank)
-        x = (torch.rand(n, d, device="cuda", generator=g) * 2 - 1).bfloat16()
-        dy = (torch.rand(n, d, device="cuda", generator=g) * 2 - 1).bfloat16()
+        x = (torch.rand(n, d, device="cuda", generator=g) * 2 - 1).to(dt)
+        dy = (torch.rand(n, d, device="cuda", generator=g) * 2 - 1).to(dt)
+        es = x.element_size()
         y = torch.empty_like(x)
         dx = torch.empty_like(x)
         if wl == "cfg5":
@@ -433,7 +455,7 @@ def run_ours(args, world, rank, cfg):
 
         # ---- end to end through the public host-buffer entry point (single layers)
         e2e = None
-        if wl in ("cfg2", "cfg3"):
+        if wl in ("cfg1", "cfg2", "cfg3"):
             e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
             hx = x.cpu().pin_memory()
             hdy = dy.cpu().pin_memory()
@@ -515,13 +537,13 @@ def run_ours(args, world, rank, cfg):
             hy.copy_(xb[0], non_blocking=True)
             c2.record(stream)
             torch.cuda.synchronize()
-            h2d_gbs = n * d * 2 / (c0.elapsed_time(c1) / 1e3) / 1e9
-            d2h_gbs = n * d * 2 / (c1.elapsed_time(c2) / 1e3) / 1e9
-            pcie_cap = tokens / max(2 * n * d * 2 / (h2d_gbs * 1e9), 2 * n * d * 2 / (d2h_gbs * 1e9))
-            e2e = {"value": tokens / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 2 * n * d * 2,
-                   "d2h_bytes_per_step": 2 * n * d * 2,
+            h2d_gbs = n * d * es / (c0.elapsed_time(c1) / 1e3) / 1e9
+            d2h_gbs = n * d * es / (c1.elapsed_time(c2) / 1e3) / 1e9
+            pcie_cap = tokens / max(2 * n * d * es / (h2d_gbs * 1e9), 2 * n * d * es / (d2h_gbs * 1e9))
+            e2e = {"value": tokens / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 2 * n * d * es,
+                   "d2h_bytes_per_step": 2 * n * d * es,
                    "sync_call_value": tokens / (sync_ms / 1e3),
-                   "note": ("the PCIe traffic of a step (256 MiB each way) hides under the kernels of the "
+                   "note": (f"the PCIe traffic of a step ({2 * n * d * es >> 20} MiB each way) hides under the kernels of the "
                             "neighbouring steps, so the host loop runs at the device-resident rate; the "
                             "device-resident loop additionally records its per-stage CUDA events; "
                             "sync_call_value: one fmoe_layer_step_host call per step, results on the host "
@@ -534,7 +556,7 @@ def run_ours(args, world, rank, cfg):
                                          "H2D / D2H rates measured here cap the host-buffer path at this rate "
                                          "however fast the kernels get (DESIGN.md §6)"),
                    "training_loop": {"value": tokens / (tl_ms / 1e3), "unit": UNIT,
-                                     "h2d_bytes_per_step": n * d * 2, "d2h_bytes_per_step": 4,
+                                     "h2d_bytes_per_step": n * d * es, "d2h_bytes_per_step": 4,
                                      "path": ("MoELayer.forward/backward: x uploaded from pinned host memory each "
                                               "step (copy stream, double-buffered), d_y device-resident, d_x left "
                                               "on the device, one fp32 scalar (sum of y) read back per step")}}
@@ -546,7 +568,13 @@ def run_ours(args, world, rank, cfg):
     flop_gemm = 2.0 * n * k * d * h
     gemm_ms = [stage_ms[s] for s in GEMM_STAGES]
     avg_launch_ms = sum(gemm_ms) / len(gemm_ms)
-    achieved = flop_gemm / (avg_launch_ms / 1e3) / 1e12
+    if avg_launch_ms <= 0:  # no per-GEMM stage marks on this path (FMOE_F32_SIMT)
+        avg_launch_ms = float("nan")
+    # cfg1 (FMOE_F32): each expert GEMM is 3 bf16 passes on the tensor pipe
+    # (bf16x3 split products, f32x.cu); the roofline counts the pipe's work,
+    # algorithmic_fp32_tflops the fp32 FLOPs the layer delivers
+    passes = 3 if wl == "cfg1" else 1
+    achieved = passes * flop_gemm / (avg_launch_ms / 1e3) / 1e12
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp) and wl == "cfg2":
@@ -554,13 +582,13 @@ def run_ours(args, world, rank, cfg):
             traffic = json.load(open(tp)).get("tc_gemm_dram_bytes_per_launch")
         except Exception:
             traffic = None
-    s = 2  # bf16
+    s = es
     scatter_bytes = s * d * (n + n * k) + 4 * n * k
     gather_bytes = s * d * (n * k + n) + 8 * n * k
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "ms_per_step_stddev": ms_sd, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32" if wl == "cfg1" else "bf16",
         "data": "synthetic (uniform[-1,1) inputs; reference init_state weights"
                 + ("; injected Zipf routing" if wl == "cfg5" else "") + ")",
         "config": {"workload": workload_name(wl, cfg, world), "n_b_per_gpu": n, "d_m": d, "d_h": h,
@@ -585,6 +613,12 @@ def run_ours(args, world, rank, cfg):
                      "peak_source": pk["src"] + " bf16, " + peak_why,
                      "per_gemm_tflops": {s_: round(flop_gemm / (stage_ms[s_] / 1e3) / 1e12, 1)
                                          for s_ in GEMM_STAGES if stage_ms[s_] > 0},
+                     **({"algorithmic_fp32_tflops": flop_gemm / (avg_launch_ms / 1e3) / 1e12,
+                         "bf16_passes_per_gemm": passes,
+                         "note": ("FMOE_F32: fp32 operands split into bf16 hi/lo planes, each GEMM = hi*lo' + lo*hi' + "
+                                  "hi*hi' on tcgen05 into one fp32 accumulator (3 bf16 passes); 'achieved' counts the "
+                                  "tensor pipe's bf16 work, per_gemm_tflops the fp32 FLOPs; stage times include the "
+                                  "hi/lo split passes of the stage's operands")} if passes > 1 else {}),
                      **({"note": ("averaged over the six expert GEMMs; with few rows per expert the weight-gradient "
                                   "launches are bound by writing fp32 gradients (HBM), not by the tensor pipe "
                                   "(profiles/r01h_cfg4_wgrad.md); fc1/fc2/dgrad stages in stages_ms")}

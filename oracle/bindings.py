@@ -530,3 +530,23 @@ ref = Ref()
 
 def ref_available() -> bool:
     return os.path.exists(REF_SO)
+
+
+REF_SO_V4 = os.path.join(HERE, "_ref", "libfmoe_ref_v4.so")
+
+
+def host_has_avx512() -> bool:
+    try:
+        flags = open("/proc/cpuinfo").read().split("flags", 2)[1].split("\n", 1)[0].split()
+    except (OSError, IndexError):
+        return False
+    return all(f in flags for f in ("avx512f", "avx512bw", "avx512cd", "avx512dq", "avx512vl"))
+
+
+def ref_timing_so() -> tuple[str, str]:
+    """The reference build to TIME on this host (bench.py's CPU arm): the
+    x86-64-v4 (AVX-512) build when the host has AVX-512 -- the nearest
+    portable equivalent of the reference's -march=native -- else the v3 one."""
+    if os.path.exists(REF_SO_V4) and host_has_avx512():
+        return REF_SO_V4, "-O3 -march=x86-64-v4 (AVX-512; host has avx512f/bw/cd/dq/vl)"
+    return REF_SO, "-O3 -march=x86-64-v3 (AVX2+FMA)"

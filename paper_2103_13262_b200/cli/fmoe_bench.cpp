@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -56,6 +58,7 @@ struct Opts {
   int reps = 16, warmup = 2, world = 1, steps = 20;
   double lr = 0.05;
   std::string out, dtype = "bf16";
+  std::string api = "device";  // bench-local: device (C-ABI layer) | reference (fmoe::forward/backward)
 };
 
 fmoe_dtype dtype_of(const std::string& s) {
@@ -103,6 +106,7 @@ Opts parse(int argc, char** argv, int first) {
     else if (a == "--steps") o.steps = std::stoi(val());
     else if (a == "--lr") o.lr = std::stod(val());
     else if (a == "--dtype") o.dtype = val();
+    else if (a == "--api") o.api = val();
     else throw Fail(2, "unknown flag " + a);
   }
   if (o.reps < 1 || o.warmup < 0 || o.world < 1) throw Fail(2, "--reps >= 1, --warmup >= 0, --world >= 1");
@@ -233,7 +237,58 @@ Timing measure(Rank& r, int warmup, int reps, F&& fn) {
 }
 
 // ------------------------------------------------------------ subcommands
+// bench-local --api reference: the reference's own moe_batched_forward /
+// moe_batched_fwdbwd loops (fmoe_bench.cpp:210-253, host steady_clock timing)
+// over its C++ API -- init_state, forward, backward of include/fmoe/
+// moe_layer.hpp with host Matrix values -- served by libfmoe_dropin.so on the
+// GPU in FMOE_F64 (bit-identical to the reference library), weights resident
+// on the device between calls.
+template <typename F>
+Timing measure_host(int warmup, int reps, F&& fn) {
+  for (int i = 0; i < warmup; ++i) fn();
+  std::vector<double> s;
+  for (int i = 0; i < reps; ++i) {
+    const auto t0 = std::chrono::steady_clock::now();
+    fn();
+    s.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
+  Timing t;
+  for (double v : s) t.mean_ms += v;
+  t.mean_ms /= reps;
+  double var = 0;
+  for (double v : s) var += (v - t.mean_ms) * (v - t.mean_ms);
+  t.stddev_ms = reps > 1 ? std::sqrt(var / (reps - 1)) : 0.0;
+  return t;
+}
+
+int bench_local_reference_api(const Opts& o) {
+  Csv csv(o.out);
+  csv.out() << hardware_line()
+            << "\n# api: reference C++ API (fmoe::init_state / forward / backward, include/fmoe/moe_layer.hpp) "
+               "through libfmoe_dropin.so, FMOE_F64, host timing\n"
+            << kCsvHeader << "\n";
+  for (size_t n_e : o.n_e_list) {
+    if (n_e == 0 || o.k > n_e) throw Fail(2, "bench-local: need 1 <= k <= n_e");
+    const fmoe::MoEConfig config{o.n_b, o.d_m, o.d_h, o.k, n_e, 1, o.seed};
+    const fmoe::MoELayerState state = fmoe::init_state(config);
+    const fmoe::Matrix x = seeded(o.seed, 102, o.n_b, o.d_m);
+    const fmoe::Matrix d_y = seeded(o.seed, 103, o.n_b, o.d_m);
+    fmoe::Matrix sink;
+    const Timing fwd = measure_host(o.warmup, o.reps, [&] { sink = fmoe::forward(x, state); });
+    row(csv.out(), "moe_batched_forward", o, n_e, 1, fwd, flops_fwd(o, n_e));
+    const Timing both = measure_host(o.warmup, o.reps, [&] {
+      fmoe::MoEForwardCache cache;
+      sink = fmoe::forward(x, state, nullptr, &cache);
+      fmoe::backward(d_y, cache, state);
+    });
+    row(csv.out(), "moe_batched_fwdbwd", o, n_e, 1, both, flops_fwd(o, n_e) + flops_bwd(o, n_e));
+  }
+  return 0;
+}
+
 int bench_local(const Opts& o) {
+  if (o.api == "reference") return bench_local_reference_api(o);
+  if (o.api != "device") throw Fail(2, "--api must be device or reference");
   const fmoe_dtype t = dtype_of(o.dtype);
   Csv csv(o.out);
   csv.out() << hardware_line() << "\n# dtype: " << o.dtype << ", device timing (CUDA events)\n" << kCsvHeader << "\n";
@@ -371,7 +426,7 @@ int train_toy(const Opts& o) {
 int usage() {
   std::cerr << "usage: fmoe_bench {bench-local|bench-dist|train-toy} [--n-b N --d-m D --d-h H --k K --n-e E[,E..]\n"
                "                  --seed S --reps R --warmup W --out FILE --world W --steps T --lr LR\n"
-               "                  --dtype bf16|f32|f64]\n";
+               "                  --dtype bf16|f32|f64] [bench-local: --api device|reference]\n";
   return 2;
 }
 

@@ -87,6 +87,7 @@ int fmoe_ctx_destroy(fmoe_ctx* ctx) {
     cudaFree(c->d_error);
     if (c->d_probe) cudaFree(c->d_probe);
     if (c->ws) cudaFree(c->ws);
+    if (c->pws) cudaFree(c->pws);
     if (c->copy_in) cudaStreamDestroy(c->copy_in);
     if (c->copy_out) cudaStreamDestroy(c->copy_out);
     for (auto e : c->ev_io)

@@ -66,6 +66,8 @@ struct Ctx {
   bool owns_transport = true;
   void* ws = nullptr;      // grow-only scratch for operator-level calls
   size_t ws_size = 0;
+  void* pws = nullptr;     // grow-only bf16x3 operand planes of operator-level FMOE_F32 calls (f32x.cu)
+  size_t pws_size = 0;
   int world = 1, rank = 0;
   Prof* prof = nullptr;
   int prof_slot = -1;      // slot of the layer step being issued (-1: none)

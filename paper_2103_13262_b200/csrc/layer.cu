@@ -84,7 +84,11 @@ Layer::Layer(Ctx* c, const fmoe_layer_config& cf) : ctx(c), cfg(cf) {
   const bool ep_mode = cfg.world_size > 1;  // EP: plan/xs/ys are the send layout
   // bf16 expert blocks: 256-row aligned (CTA-pair GEMM tiles) when experts
   // average >= 1024 rows, else 128 (single-CTA tiles waste less padding)
-  plan.align = (bf && !ep_mode) ? expert_block_align(n * k, E) : 1;
+  // FMOE_F32 runs its expert GEMMs on the tensor cores (bf16x3, f32x.cu) over
+  // the same aligned blocks; FMOE_F32_SIMT=1 keeps the reference layout and
+  // the SIMT fp32 kernels
+  const bool f32tc = t == FMOE_F32 && !ep_mode && f32_tc_enabled() && d % 64 == 0 && h % 64 == 0 && E % 8 == 0;
+  plan.align = ((bf || f32tc) && !ep_mode) ? expert_block_align(n * k, E) : 1;
   plan.capacity = plan_capacity(n, k, E, plan.align);
   plan.counts = dalloc<int32_t>(owned, E);
   plan.offsets = dalloc<int32_t>(owned, E + 1);
@@ -112,6 +116,7 @@ Layer::Layer(Ctx* c, const fmoe_layer_config& cf) : ctx(c), cfg(cf) {
   part = dalloc<float>(owned, S * d * E + S + 64);
   if (!ep_mode) tpart = dalloc<float>(owned, experts_bwd_part_floats(plan, d, h));
   if (!ep_mode && bf) relu_bits = dalloc<uint32_t>(owned, cap * (h / 32));
+  if (f32tc) f32_planes = dalloc<__nv_bfloat16>(owned, f32_planes_elems(n, d, h, E, el, cap));
   if (cfg.world_size > 1) ep_alloc();
 }
 
@@ -122,6 +127,11 @@ Layer::~Layer() {
       if (evs[s]) cudaEventDestroy(evs[s]);
   for (void* p : owned) cudaFree(p);
   if (h_stage) cudaFreeHost(h_stage);
+}
+
+F32Planes Layer::planes_view() const {
+  if (!f32_planes) return F32Planes{};
+  return f32_planes_at(f32_planes, cfg.n_b, cfg.d_m, cfg.d_h, E, cfg.n_e_local, plan.capacity);
 }
 
 fmoe_expert_params Layer::params() const { return fmoe_expert_params{w1, b1, w2, b2}; }
@@ -163,7 +173,11 @@ void Layer::forward(const void* x, void* y) {
   routed = false;
   prof_slot = ctx_take_slot(ctx);
   ctx_mark(ctx, MARK_FWD_BEGIN);
-  gate_fwd(ctx, t, x, wg, n, d, E, k, scores, idx, vals, logits);  // gate.cpp:23-35
+  if (f32_planes)  // FMOE_F32 on the tensor cores: logits as a bf16x6 product (f32x.cu)
+    gate_fwd_f32tc(ctx, (const float*)x, (const float*)wg, n, d, E, k, (float*)scores, idx, (float*)vals,
+                   (float*)logits, planes_view());
+  else
+    gate_fwd(ctx, t, x, wg, n, d, E, k, scores, idx, vals, logits);  // gate.cpp:23-35
   ctx_mark(ctx, MARK_GATE);
   dispatch_and_experts(x, y);
 }
@@ -211,7 +225,9 @@ void Layer::dispatch_and_experts(const void* x, void* y) {
   ctx_mark(ctx, MARK_PLAN);
   scatter(ctx, t, x, d, plan, xs);                                // dispatch.cpp:49-59
   ctx_mark(ctx, MARK_SCATTER);
-  experts_fwd(ctx, t, plan, d, h, params(), xs, hidden, ys, relu_bits);  // expert.cpp:85-102
+  const F32Planes pv = planes_view();
+  experts_fwd(ctx, t, plan, d, h, params(), xs, hidden, ys, relu_bits, nullptr, nullptr, nullptr,
+              f32_planes ? &pv : nullptr);  // expert.cpp:85-102
   gather_combine(ctx, t, ys, d, plan, vals, y);                   // dispatch.cpp:61-78
   ctx_mark(ctx, MARK_GATHER);
   fwd_done = true;
@@ -236,8 +252,9 @@ void Layer::backward(const void* dy, void* dx, cudaEvent_t dx_ready) {
   if (routed) {  // injected routing: no gate (see forward_routed), zero gate gradient
     CK(cudaMemsetAsync(dwg, 0, (size_t)d * E * ss, ctx->stream));
     const int ph = bf ? EXPERTS_BWD_DGRAD : EXPERTS_BWD_ALL;
+    const F32Planes pv = planes_view();
     experts_bwd(ctx, t, plan, d, h, params(), xs, hidden, d_ys, d_xs, grads(), d_pre, tpart, relu_bits,
-                nullptr, ph);
+                nullptr, ph, nullptr, nullptr, f32_planes ? &pv : nullptr);
     scatter_bwd(ctx, t, d_xs, d, plan, dx, nullptr);
     ctx_mark(ctx, MARK_GATE_DX);
     if (dx_ready) CK(cudaEventRecord(dx_ready, ctx->stream));
@@ -261,9 +278,15 @@ void Layer::backward(const void* dy, void* dx, cudaEvent_t dx_ready) {
     gate_dwg_bf16(ctx, x_saved, dz_bf16, n, d, E, part, (float*)dwg);  // gate.cpp:62
     ctx_mark(ctx, MARK_GATE_DWG);
   } else {
-    experts_bwd(ctx, t, plan, d, h, params(), xs, hidden, d_ys, d_xs, grads(), d_pre, tpart,
-                relu_bits);  // expert.cpp:104-125
-    gate_bwd(ctx, t, x_saved, wg, scores, idx, d_w, n, d, E, k, dwg, gdx, dz, nullptr, nullptr);
+    const F32Planes pv = planes_view();
+    experts_bwd(ctx, t, plan, d, h, params(), xs, hidden, d_ys, d_xs, grads(), d_pre, tpart, relu_bits, nullptr,
+                EXPERTS_BWD_ALL, nullptr, nullptr, f32_planes ? &pv : nullptr);  // expert.cpp:104-125
+    if (f32_planes) {  // gate.cpp:44-63: Jacobian on SIMT fp32, d_wg / d_x as bf16x6 products
+      gate_dlogits(ctx, t, scores, idx, d_w, n, E, k, dz);
+      gate_bwd_f32tc(ctx, (const float*)dz, n, d, E, part, (float*)dwg, (float*)gdx, planes_view());
+    } else {
+      gate_bwd(ctx, t, x_saved, wg, scores, idx, d_w, n, d, E, k, dwg, gdx, dz, nullptr, nullptr);
+    }
     ctx_mark(ctx, MARK_GATE_DWG);
     scatter_bwd(ctx, t, d_xs, d, plan, dx, gdx);  // dispatch.cpp:80-95, moe_layer.cpp:140
     ctx_mark(ctx, MARK_GATE_DX);

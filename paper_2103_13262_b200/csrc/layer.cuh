@@ -33,6 +33,10 @@ struct Layer {
   float* part = nullptr;   // gate d_wg split-K partials
   float* tpart = nullptr;  // expert bias-gradient tile partials
   uint32_t* relu_bits = nullptr;  // bf16: hidden > 0 bitmap (fc1 -> dgrad fc2)
+  // FMOE_F32 on the tensor cores (f32x.cu): bf16x6 operand planes of x, Wg,
+  // dz, xs, hidden, d_ys, d_pre, W1, W2 (three each); null on the SIMT route
+  __nv_bfloat16* f32_planes = nullptr;
+  struct F32Planes planes_view() const;
   // host-buffer steps: two device buffer sets (x, y, dy, dx each) and their events
   void* io = nullptr;
   struct HostIO {

@@ -38,6 +38,11 @@ void relu_rows(Ctx* ctx, const T* in, T* out, int64_t n) {
   relu_kernel<T><<<(unsigned)ceil_div(n, 256), 256, 0, ctx->stream>>>(in, out, n);
   CK_LAUNCH(ctx);
 }
+}  // namespace
+
+void relu_rows_f32(Ctx* ctx, const float* in, float* out, int64_t n) { relu_rows<float>(ctx, in, out, n); }
+
+namespace {
 
 int pick_bn(int64_t n) { return n <= 64 ? 64 : n <= 128 ? 128 : 256; }
 
@@ -202,9 +207,14 @@ static void set_route(tc::Params& p, const RowRoute* r) {
 
 void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
                  const fmoe_expert_params& w, const void* xs, void* hidden, void* ys,
-                 uint32_t* relu_bits, void* preact, const RowRoute* ys_route, const Arrival* arrive) {
+                 uint32_t* relu_bits, void* preact, const RowRoute* ys_route, const Arrival* arrive,
+                 const F32Planes* planes) {
   const int64_t E = b.n_experts;
   if (E == 0 || b.capacity == 0) return;
+  if (t == FMOE_F32 && !ys_route && f32_tc_route(b, d, h)) {  // tensor cores, bf16x3 (f32x.cu)
+    experts_fwd_f32tc(ctx, b, d, h, w, xs, hidden, ys, preact, planes);
+    return;
+  }
   if (t == FMOE_F64 || t == FMOE_F32) {
     if (ys_route) shape_error("experts_fwd: routed outputs are bf16-only");
     const auto cnt = host_counts(ctx, b);
@@ -271,9 +281,15 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
                  const fmoe_expert_params& w, const void* xs, const void* hidden, const void* d_ys,
                  void* d_xs, const fmoe_expert_grads& g, void* d_pre, float* part_ws,
                  const uint32_t* relu_bits, const void* mask, int phase, const RowRoute* dxs_route,
-                 const Arrival* arrive) {
+                 const Arrival* arrive, const F32Planes* planes) {
   const int64_t E = b.n_experts;
   if (E == 0) return;
+  if (t == FMOE_F32 && phase == EXPERTS_BWD_ALL && !dxs_route && f32_tc_route(b, d, h)) {
+    // tensor cores, bf16x3 (f32x.cu); group order after the bias partials
+    int* order = reinterpret_cast<int*>(part_ws + (b.capacity / 128 + 1) * (d + h));
+    experts_bwd_f32tc(ctx, b, d, h, w, xs, hidden, d_ys, d_xs, g, d_pre, mask, order, planes);
+    return;
+  }
   if (t == FMOE_F64 || t == FMOE_F32) {
     if (phase != EXPERTS_BWD_ALL || dxs_route) shape_error("experts_bwd: phased / routed backward is bf16-only");
     const auto cnt = host_counts(ctx, b);

@@ -49,10 +49,18 @@ struct Arrival {
   const int* mtile_order = nullptr;
   int grid_limit = 0;
 };
+// FMOE_F32 GEMMs on the tensor cores (f32x.cu, "bf16x6"): fp32 operands
+// split into three bf16 planes ([p0: n][p1: n][p2: n]).  The layer keeps the
+// planes of x, xs, hidden and the weights from the forward for the backward;
+// per-operator expert calls pass NULL and split into context scratch.
+struct F32Planes {
+  __nv_bfloat16 *x = nullptr, *wg = nullptr, *dz = nullptr;
+  __nv_bfloat16 *xs = nullptr, *hidden = nullptr, *d_ys = nullptr, *d_pre = nullptr, *w1 = nullptr, *w2 = nullptr;
+};
 void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
                  const fmoe_expert_params& w, const void* xs, void* hidden, void* ys,
                  uint32_t* relu_bits = nullptr, void* preact = nullptr, const RowRoute* ys_route = nullptr,
-                 const Arrival* arrive = nullptr);
+                 const Arrival* arrive = nullptr, const F32Planes* planes = nullptr);
 // preact (SIMT dtypes only, optional): also keep x*w1 + b1 before the relu
 // (ForwardCache::preact, expert.hpp:31-35).
 // d_pre_ws: [capacity, h] dtype scratch; mask (SIMT dtypes only, optional): the
@@ -75,7 +83,28 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
                  void* d_xs, const fmoe_expert_grads& g, void* d_pre_ws, float* part_ws,
                  const uint32_t* relu_bits = nullptr, const void* mask = nullptr,
                  int phase = EXPERTS_BWD_ALL, const RowRoute* dxs_route = nullptr,
-                 const Arrival* arrive = nullptr);
+                 const Arrival* arrive = nullptr, const F32Planes* planes = nullptr);
+// true when an FMOE_F32 expert call takes the tensor-core route: a 128-row
+// aligned plan with its tile table, d_m and d_h multiples of 64, and
+// FMOE_F32_SIMT unset (=1 keeps the SIMT fp32 kernels, the reference's order)
+bool f32_tc_route(const fmoe_plan& b, int64_t d, int64_t h);
+bool f32_tc_enabled();
+void split_bf16x3(Ctx* ctx, const float* src, __nv_bfloat16* planes, int64_t n);
+// a layer's planes: element count and carving of one allocation
+int64_t f32_planes_elems(int64_t n, int64_t d, int64_t h, int64_t e, int64_t el, int64_t cap);
+F32Planes f32_planes_at(__nv_bfloat16* base, int64_t n, int64_t d, int64_t h, int64_t e, int64_t el, int64_t cap);
+// the layer's gate products on the tensor cores (softmax / top-k / Jacobian on SIMT fp32)
+void gate_fwd_f32tc(Ctx* ctx, const float* x, const float* wg, int64_t n, int64_t d, int64_t e, int64_t k,
+                    float* scores, int32_t* idx, float* vals, float* logits, const F32Planes& pl);
+void gate_bwd_f32tc(Ctx* ctx, const float* dz, int64_t n, int64_t d, int64_t e, float* part_ws, float* d_wg,
+                    float* d_x, const F32Planes& pl);
+void experts_fwd_f32tc(Ctx* ctx, const fmoe_plan& b, int64_t d, int64_t h, const fmoe_expert_params& w,
+                       const void* xs, void* hidden, void* ys, void* preact, const F32Planes* pl);
+void experts_bwd_f32tc(Ctx* ctx, const fmoe_plan& b, int64_t d, int64_t h, const fmoe_expert_params& w,
+                       const void* xs, const void* hidden, const void* d_ys, void* d_xs, const fmoe_expert_grads& g,
+                       void* d_pre, const void* mask, int* group_order, const F32Planes* pl);
+void relu_rows_f32(Ctx* ctx, const float* in, float* out, int64_t n);
+
 // allreduce_sum over ctx's transport (ep.cu): in place, ascending-rank order.
 void allreduce_sum(Ctx* c, fmoe_dtype dt, void* buf, int64_t n, const int* group, int64_t gs);
 

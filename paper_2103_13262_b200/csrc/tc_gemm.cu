@@ -18,17 +18,18 @@ struct Cfg {
   static constexpr int B_BYTES = (BN / CG) * BK * 2;   // this CTA's share of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;             // two fp32 accumulators
-  static constexpr int COLSUM_BYTES = EPI == EPI_F32 ? 0 : 4 * BN * 4;  // per-warp column sums of one tile
+  static constexpr bool F32OUT = EPI == EPI_F32 || EPI == EPI_F32X;  // fp32 output tiles
+  static constexpr int COLSUM_BYTES = F32OUT ? 0 : 4 * BN * 4;  // per-warp column sums of one tile
   // outputs leave through TMA stores from per-warp staging tiles of 32 rows x
   // 64 B (64B swizzle): 32 bf16 columns, or 16 fp32 columns (a 32-column fp32
   // chunk is stored as two halves).  One tile per warp keeps 6 pipeline
   // stages in shared memory.
-  static constexpr bool TMA_STORE = EPI == EPI_BF16 || EPI == EPI_MASK_BF16 || EPI == EPI_F32;
+  static constexpr bool TMA_STORE = EPI == EPI_BF16 || EPI == EPI_MASK_BF16 || F32OUT;
 #ifndef FMOE_TC_F32_ROW_BYTES
 #define FMOE_TC_F32_ROW_BYTES 64  // fp32 staging rows: 64 B (16 columns, two stores per chunk); 128 B
                                   // (one 32-column store) measured 5% slower weight gradients
 #endif
-  static constexpr int OUT_ROW_BYTES = EPI == EPI_F32 ? FMOE_TC_F32_ROW_BYTES : 64;
+  static constexpr int OUT_ROW_BYTES = F32OUT ? FMOE_TC_F32_ROW_BYTES : 64;
 #ifndef FMOE_TC_BF16_NBUF
 #define FMOE_TC_BF16_NBUF 1  // staging tiles per epilogue warp for bf16 outputs (A/B: 2 tiles cost a
                              // pipeline stage or the 227 KB plan; both measured slower overall)
@@ -36,7 +37,7 @@ struct Cfg {
 #ifndef FMOE_TC_F32_NBUF
 #define FMOE_TC_F32_NBUF 1  // staging tiles per epilogue warp for fp32 (weight-gradient) outputs
 #endif
-  static constexpr int NBUF = EPI == EPI_F32 ? FMOE_TC_F32_NBUF : FMOE_TC_BF16_NBUF;
+  static constexpr int NBUF = F32OUT ? FMOE_TC_F32_NBUF : FMOE_TC_BF16_NBUF;
   static constexpr int TILE_BYTES = 32 * OUT_ROW_BYTES;
   static constexpr int STORE_BYTES = TMA_STORE ? 8 * NBUF * TILE_BYTES : 0;
   // bf16 epilogues stage the bias of each warp's 128-column slice of the tile
@@ -49,7 +50,7 @@ struct Cfg {
 #define FMOE_TC_F32_SMEM_KB FMOE_TC_SMEM_KB
 #endif
   static constexpr int BUDGET =
-      (EPI == EPI_F32 ? FMOE_TC_F32_SMEM_KB : FMOE_TC_SMEM_KB) * 1024 - 1280 /*align + barriers*/ - STORE_BYTES - COLSUM_BYTES - BIAS_BYTES;
+      (F32OUT ? FMOE_TC_F32_SMEM_KB : FMOE_TC_SMEM_KB) * 1024 - 1280 /*align + barriers*/ - STORE_BYTES - COLSUM_BYTES - BIAS_BYTES;
   static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
   static constexpr int SMEM =
       STAGES * STAGE_BYTES + STORE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + COLSUM_BYTES + BIAS_BYTES;
@@ -96,7 +97,8 @@ __device__ __forceinline__ constexpr uint32_t idesc() {
 }
 
 struct Tile {
-  int g, m0, n0, kbeg, nkb;  // m0: first row of the (pair) tile
+  int g, m0, n0, kbeg, nkb;  // m0: first row of the (pair) tile; nkb: k-blocks of all phases
+  int kpp;                   // k-blocks per phase (bf16x3: nkb = 3 * kpp)
 };
 
 template <int BN>
@@ -116,7 +118,7 @@ __device__ __forceinline__ int total_tiles(const Params& p) {
   return p.n_groups * ((p.M + BM * CG - 1) / (BM * CG)) * nn;
 }
 
-template <int BN, int CG>
+template <int BN, int CG, bool SPLIT = false>
 __device__ __forceinline__ Tile decode(const Params& p, int t) {
   Tile r;
   const int nn = n_tiles_n<BN>(p);
@@ -127,7 +129,7 @@ __device__ __forceinline__ Tile decode(const Params& p, int t) {
     r.m0 = mt * BM * CG;
     r.g = p.tile_group ? __ldg(p.tile_group + mt * CG) : 0;
     r.kbeg = 0;
-    r.nkb = (p.K + BK - 1) / BK;
+    r.kpp = (p.K + BK - 1) / BK;
   } else {
     const int nm = (p.M + BM * CG - 1) / (BM * CG);
     const int per = nm * nn;
@@ -145,8 +147,9 @@ __device__ __forceinline__ Tile decode(const Params& p, int t) {
       r.kbeg = r.g * p.k_split;
       kend = min(p.K, r.kbeg + p.k_split);
     }
-    r.nkb = (kend - r.kbeg + BK - 1) / BK;
+    r.kpp = (kend - r.kbeg + BK - 1) / BK;
   }
+  r.nkb = (SPLIT && p.phases > 1) ? r.kpp * p.phases : r.kpp;  // split passes: fp32-output kernels only
   return r;
 }
 
@@ -176,7 +179,7 @@ __device__ __forceinline__ void epi_store_chunk(const Params& p, const Tile& tl,
                                                 float (&v)[32], uint32_t bits = 0,
                                                 uint32_t stage_addr = 0) {
   // row: absolute row in the output tile space; c0: absolute column of v[0]
-  if constexpr (EPI == EPI_F32) {
+  if constexpr (EPI == EPI_F32 || EPI == EPI_F32X) {
     float* out = reinterpret_cast<float*>(p.C) + (int64_t)tl.g * p.c_group_stride +
                  (int64_t)row * p.ldc + c0;
     if (row >= p.M) return;
@@ -582,7 +585,8 @@ __device__ __forceinline__ void wait_rows_arrived(const Params& p, int g, int r0
 template <int BN, bool A_MN, bool B_MN, int CG, int EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmC, const Params p) {
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ SplitMaps tmS,
+                   const Params p) {
   using C = Cfg<BN, CG, EPI>;
   constexpr int STAGES = C::STAGES;
   // CTA pair (CG=2): rank 0 (leader) issues the MMAs for both CTAs; both
@@ -614,6 +618,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
+    if (C::F32OUT && p.phases > 1) {
+      prefetch_tmap(&tmS.a1);
+      prefetch_tmap(&tmS.a2);
+      prefetch_tmap(&tmS.b1);
+      prefetch_tmap(&tmS.b2);
+    }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(smem_u32(full + s), 1);
       mbar_init(smem_u32(empty + s), 1);
@@ -657,10 +667,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int it = 0; it * tstep < total; ++it) {
         const int t = tile_at(p, it, t0, tstep);
         if (t >= total) continue;
-        const Tile tl = decode<BN, CG>(p, t);
+        const Tile tl = decode<BN, CG, C::F32OUT>(p, t);
         const int brow = (p.mode == RAGGED_M) ? tl.g * p.b_group_rows : tl.kbeg;
         if (p.arrive_flags && tl.nkb > 0) wait_rows_arrived(p, tl.g, tl.m0 + row_off, lane);
-        for (int kb = 0; kb < tl.nkb; ++kb) {
+        // split (bf16x6) passes: kb restarts at 0 for every pass, whose A / B
+        // planes come from sel_a / sel_b
+        int ph = 0;
+        for (int kb = 0, kbt = 0; kbt < tl.nkb; ++kbt) {
+          const CUtensorMap* mA = &tmA;
+          const CUtensorMap* mB = &tmB;
+          if constexpr (C::F32OUT) {
+            if (tl.kpp != tl.nkb) {
+              const uint32_t pa = (p.sel_a >> (4 * ph)) & 3u, pb = (p.sel_b >> (4 * ph)) & 3u;
+              mA = pa == 0 ? &tmA : pa == 1 ? &tmS.a1 : &tmS.a2;
+              mB = pb == 0 ? &tmB : pb == 1 ? &tmS.b1 : &tmS.b2;
+            }
+          }
           mbar_wait(smem_u32(empty + stage), phase ^ 1);
           const uint32_t fb = smem_u32(full + stage);
           if (rank == 0) {
@@ -680,22 +702,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               tma_load_2d(dst, m, fb, c0, c1);
           };
           if (!A_MN) {
-            load(a_dst, &tmA, kb * BK, tl.m0 + row_off);
+            load(a_dst, mA, kb * BK, tl.m0 + row_off);
           } else {
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j)
-              load(a_dst + j * 8192, &tmA, tl.m0 + row_off + 64 * j, tl.kbeg + kb * BK);
+              load(a_dst + j * 8192, mA, tl.m0 + row_off + 64 * j, tl.kbeg + kb * BK);
           }
           if (!B_MN) {
-            load(b_dst, &tmB, kb * BK, brow + tl.n0 + n_off);
+            load(b_dst, mB, kb * BK, brow + tl.n0 + n_off);
           } else {
 #pragma unroll
             for (int j = 0; j < BN / CG / 64; ++j)
-              load(b_dst + j * 8192, &tmB, tl.n0 + n_off + 64 * j, brow + kb * BK);
+              load(b_dst + j * 8192, mB, tl.n0 + n_off + 64 * j, brow + kb * BK);
           }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
+          }
+          if (++kb == tl.kpp) {
+            kb = 0;
+            ++ph;
           }
         }
       }
@@ -719,7 +745,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int it = 0; it * tstep < total; ++it) {
         const int t = tile_at(p, it, t0, tstep);
         if (t >= total) continue;
-        const Tile tl = decode<BN, CG>(p, t);
+        const Tile tl = decode<BN, CG, C::F32OUT>(p, t);
         if (tl.nkb == 0) continue;
         mbar_wait(smem_u32(tempty + acc), acc_phase ^ 1);
         tc_fence_after();
@@ -780,7 +806,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int it = 0; it * tstep < total; ++it) {
       const int t = tile_at(p, it, t0, tstep);
       if (t >= total) continue;
-      const Tile tl = decode<BN, CG>(p, t);
+      const Tile tl = decode<BN, CG, C::F32OUT>(p, t);
       const int row = tl.m0 + row_off + q * 32 + lane;
       if (tl.nkb == 0) {
         // empty K range (expert without tokens): gradient is exactly zero
@@ -924,7 +950,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             float v[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(buf[i & 1][j]);
-            if constexpr (EPI == EPI_F32) {
+            if constexpr (EPI == EPI_F32X) {
+              // fp32 expert outputs (FMOE_F32): dot product, then the rounded
+              // bias add, relu keeping -0.0, strict > 0 mask -- the SIMT
+              // kernel's order (gemm_simt.cu, matrix.cpp:128-153)
+              const int c0 = tl.n0 + c * 32;
+              if (row < p.M) {
+                if (p.bias) {
+                  const float* bb = p.bias + (int64_t)tl.g * p.bias_group_stride + c0;
+#pragma unroll
+                  for (int j = 0; j < 32; ++j)
+                    if (c0 + j < p.N) v[j] = v[j] + __ldg(bb + j);
+                }
+                if (p.relu) {
+#pragma unroll
+                  for (int j = 0; j < 32; ++j) v[j] = v[j] < 0.f ? 0.f : v[j];
+                }
+                if (p.maskf) {
+                  const float* mr = p.maskf + (int64_t)row * p.ldm + c0;
+#pragma unroll
+                  for (int j = 0; j < 32; ++j)
+                    if (c0 + j < p.N) v[j] = __ldg(mr + j) > 0.f ? v[j] : 0.f;
+                }
+              }
+            }
+            if constexpr (C::F32OUT) {
               if (p.tma_out) {
                 // fp32 staging (rows >= M staged as zeros, clipped by the tensor map):
                 //  64 B rows: two 16-column halves, 64B swizzle (16-byte chunk j of row r
@@ -1067,7 +1117,7 @@ CUtensorMap make_tmap(const void* base, uint64_t inner, uint64_t outer, uint64_t
 
 template <int BN, bool A_MN, bool B_MN, int CG, int EPI>
 static void launch_t(Ctx* ctx, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
-                     int64_t max_tiles) {
+                     int64_t max_tiles, const SplitMaps* split) {
   auto kern = tc_gemm_kernel<BN, A_MN, B_MN, CG, EPI>;
   using C = Cfg<BN, CG, EPI>;
   // Output tensor map for the TMA-store epilogue: 32x32 boxes matching the
@@ -1077,7 +1127,7 @@ static void launch_t(Ctx* ctx, const CUtensorMap& ta, const CUtensorMap& tb, con
   q.tma_out = 0;
   CUtensorMap tc_out = ta;
   if (C::TMA_STORE) {
-    if (EPI == EPI_F32) {
+    if (C::F32OUT) {
       const bool grouped = p.c_group_stride != 0;
       const bool ok = p.ldc == p.N && (p.N % 4) == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 &&
                       (!grouped || (p.M % (BM * CG) == 0 && p.c_group_stride == (int64_t)p.M * p.ldc));
@@ -1111,17 +1161,19 @@ static void launch_t(Ctx* ctx, const CUtensorMap& ta, const CUtensorMap& tb, con
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc_out, q));
+  if (q.phases > 1 && (!split || !C::F32OUT)) shape_error("tc gemm: split product without its planes / fp32 output");
+  const SplitMaps sm = split ? *split : SplitMaps{ta, ta, tb, tb};
+  CK(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc_out, sm, q));
   CK_LAUNCH(ctx);
 }
 
 // Only the (tile, operand-major, CTA-group, epilogue) combinations the MoE layer uses
 // are instantiated; each kernel carries exactly one epilogue.
 void launch(Ctx* ctx, int bn, bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
-            const Params& p, int64_t max_tiles, int cg) {
+            const Params& p, int64_t max_tiles, int cg, const SplitMaps* split) {
 #define FMOE_TC_CASE(BN_, AM, BM_, CG_, EPI_)                                   \
   if (bn == BN_ && a_mn == AM && b_mn == BM_ && cg == CG_ && p.epi == EPI_) {   \
-    launch_t<BN_, AM, BM_, CG_, EPI_>(ctx, ta, tb, p, max_tiles);               \
+    launch_t<BN_, AM, BM_, CG_, EPI_>(ctx, ta, tb, p, max_tiles, split);        \
     return;                                                                     \
   }
   // expert pool, CTA pairs (256-row aligned plans)
@@ -1134,12 +1186,21 @@ void launch(Ctx* ctx, int bn, bool a_mn, bool b_mn, const CUtensorMap& ta, const
   FMOE_TC_CASE(256, false, false, 1, EPI_MASK_BF16)
   FMOE_TC_CASE(256, false, false, 1, EPI_BF16)
   FMOE_TC_CASE(256, true, true, 1, EPI_F32)
+  // FMOE_F32 expert GEMMs on the tensor cores (bf16x6, fp32 outputs; the
+  // weight gradients and gate products reuse the EPI_F32 instances)
+  FMOE_TC_CASE(256, false, true, 2, EPI_F32X)        // fc1 (+bias, relu), fc2 (+bias)
+  FMOE_TC_CASE(256, false, false, 2, EPI_F32X)       // dgrad fc2 (*mask), dgrad fc1
+  FMOE_TC_CASE(256, false, true, 1, EPI_F32X)
+  FMOE_TC_CASE(256, false, false, 1, EPI_F32X)
   // gate
   FMOE_TC_CASE(64, false, true, 1, EPI_GATE)         // logits + softmax + top-k, E <= 64
   FMOE_TC_CASE(128, false, true, 1, EPI_GATE)        // E <= 128
   FMOE_TC_CASE(256, false, true, 1, EPI_GATE)        // E <= 256
   FMOE_TC_CASE(256, false, true, 1, EPI_F32)         // logits only, E > 256
   FMOE_TC_CASE(256, false, false, 1, EPI_GATE_DX)    // gate d_x + scatter_backward
+  FMOE_TC_CASE(64, false, true, 1, EPI_F32)          // FMOE_F32 gate logits, E <= 64
+  FMOE_TC_CASE(128, false, true, 1, EPI_F32)         // FMOE_F32 gate logits, E <= 128
+  FMOE_TC_CASE(256, false, false, 1, EPI_F32)        // FMOE_F32 gate d_x
   FMOE_TC_CASE(64, true, true, 1, EPI_F32)           // gate d_wg split-K partials
   FMOE_TC_CASE(128, true, true, 1, EPI_F32)
 #undef FMOE_TC_CASE

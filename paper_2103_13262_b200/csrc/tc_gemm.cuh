@@ -46,7 +46,23 @@ enum Epi : int {
   EPI_F32 = 2,        // C = acc (fp32)                         weight gradients
   EPI_GATE = 3,       // softmax + top-k over the row           gate forward
   EPI_GATE_DX = 4,    // C = bf16(sum_j d_xs[pos(i,j)] + acc)   scatter_backward + gate d_x
+  EPI_F32X = 5,       // C = acc [+ bias] [relu] [* (maskf > 0)] (fp32)   FMOE_F32 expert GEMMs
 };
+
+// FMOE_F32 on the tensor cores ("bf16x6"): every fp32 operand is stored as
+// three bf16 planes, a0 = bf16(a), a1 = bf16(a - a0), a2 = bf16(a - a0 - a1)
+// (each difference exact in fp32; a = a0 + a1 + a2 + r, |r| <= 2^-24 |a|), and
+// a product runs as six bf16 passes over the whole K range into one fp32 TMEM
+// accumulator -- a0*b2, a2*b0, a1*b1, a0*b1, a1*b0, then a0*b0 (small terms
+// first).  The omitted a1*b2, a2*b1, a2*b2 and residual terms are <= ~2^-24 of
+// each product: fp32-class accuracy at the cost of 6 bf16 GEMMs.  (Two planes
+// and three passes leave ~1e-5 relative error per product -- enough to flip
+// relu masks near zero and miss SURVEY 8(c)'s 1e-4 gradient bound, measured.)
+// Params.phases = 6 with sel_a / sel_b (plane of each pass, one nibble per
+// pass) selects it; planes 1, 2 come in through SplitMaps.
+constexpr int SPLIT_PASSES = 6;
+constexpr uint32_t SPLIT_SEL_A = 0x010120u;  // passes 0..5 (low nibble first): 0 2 1 0 1 0
+constexpr uint32_t SPLIT_SEL_B = 0x001102u;  //                                  2 0 1 1 0 0
 
 struct Params {
   int mode;
@@ -110,6 +126,15 @@ struct Params {
   // globaltimer) at its start and end
   unsigned long long* probe;
   int tma_out;  // set by launch(): outputs leave through TMA stores
+  // bf16x6 (FMOE_F32, fp32-output epilogues only): 1 = plain bf16 GEMM
+  // (default, 0 reads as 1); > 1 = that many passes over the whole K range,
+  // pass i contracting plane (sel_a >> 4i) & 3 of A with plane (sel_b >> 4i) & 3
+  // of B
+  int phases;
+  uint32_t sel_a, sel_b;
+  // EPI_F32X: fp32 relu-backward operand [rows][ldm] (strict > 0; bias and
+  // relu as for EPI_BF16)
+  const float* maskf;
   // Expert parallelism over peer memory (EPI_BF16, RAGGED_M): every output row
   // is stored straight into the rank that sent it (fused global_gather,
   // collectives.cpp:205-265).  Row q of expert block g from source s -- rows
@@ -131,8 +156,12 @@ CUtensorMap make_tmap(const void* base, uint64_t inner, uint64_t outer, uint64_t
 // Host: launch.  a_mn / b_mn select MN-major operands; bn in {64,128,256};
 // cg = 2 runs CTA pairs (tcgen05 cta_group::2, 256-row tiles; RAGGED_M then
 // needs 256-row aligned expert blocks).  max_tiles counts (pair) tiles.
+// Planes 1 and 2 of the operands of a split (bf16x6) product.
+struct SplitMaps {
+  CUtensorMap a1, a2, b1, b2;
+};
 void launch(Ctx* ctx, int bn, bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
-            const Params& p, int64_t max_tiles, int cg = 1);
+            const Params& p, int64_t max_tiles, int cg = 1, const SplitMaps* split = nullptr);
 
 }  // namespace tc
 }  // namespace fmoe_b200

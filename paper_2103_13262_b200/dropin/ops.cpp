@@ -1,6 +1,7 @@
 // ops.cpp -- device plumbing and the stateless operators of the drop-in:
 // matrix primitives, generators, gate, dispatch and the expert pool
 // (reference API: proj/include/fmoe/{matrix,rng,gate,dispatch,expert}.hpp).
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -102,6 +103,11 @@ std::vector<std::int64_t> download_i32(const Buf& b, std::size_t n, const Device
 }
 
 }  // namespace dropin
+
+std::uint64_t Matrix::next_id() noexcept {
+  static std::atomic<std::uint64_t> next{1};
+  return next.fetch_add(1, std::memory_order_relaxed);
+}
 
 using dropin::Buf;
 using dropin::check;
@@ -501,6 +507,49 @@ DevPool device_pool(std::span<const ExpertParams> experts, const Shapes& s, cuda
   return P;
 }
 
+// Device residency of the expert pool: the stacked weights of the last two
+// pools a thread used stay on the device, keyed by every parameter Matrix's
+// content identity (id, version) -- a forward and its backward, and steps of
+// an unchanged state, upload the weights once instead of on every call
+// (sgd_step / train_step write the weights and so bump their versions).
+struct PoolKey {
+  std::vector<std::uint64_t> v;
+  bool operator==(const PoolKey&) const = default;
+};
+PoolKey pool_key(std::span<const ExpertParams> experts, const Shapes& s) {
+  PoolKey k;
+  k.v.reserve(experts.size() * 8 + 2);
+  k.v.push_back(s.dm);
+  k.v.push_back(s.dh);
+  for (const auto& e : experts)
+    for (const Matrix* m : {&e.w1, &e.b1, &e.w2, &e.b2}) {
+      k.v.push_back(m->content_id());
+      k.v.push_back(m->content_version());
+    }
+  return k;
+}
+const DevPool& device_pool_cached(std::span<const ExpertParams> experts, const Shapes& s, dropin::Device& d) {
+  struct Entry {
+    PoolKey key;
+    DevPool pool;
+    std::uint64_t used = 0;
+  };
+  thread_local Entry slots[2];  // after local(): destroyed before the thread's stream
+  thread_local std::uint64_t clock = 0;
+  PoolKey key = pool_key(experts, s);
+  for (Entry& e : slots)
+    if (e.used && e.key == key) {
+      e.used = ++clock;
+      return e.pool;
+    }
+  Entry& victim = slots[0].used <= slots[1].used ? slots[0] : slots[1];
+  victim.pool = DevPool{};  // free before allocating the replacement
+  victim.pool = device_pool(experts, s, d.stream);
+  victim.key = std::move(key);
+  victim.used = ++clock;
+  return victim.pool;
+}
+
 // Block plan of a pool call: counts/offsets only (align 1).
 struct DevBlocks {
   Buf counts, offsets;
@@ -542,7 +591,7 @@ MultiExpertResult multi_expert_forward(const Matrix& xs, std::span<const std::in
   Matrix pre(n, s.dh), hid(n, s.dh);
   if (n > 0) {
     auto& d = local();
-    DevPool P = device_pool(experts, s, d.stream);
+    const DevPool& P = device_pool_cached(experts, s, d);
     DevBlocks B = device_blocks(counts, off, d.stream);
     Buf dx = upload(xs, d.stream), dpre(n * s.dh * 8, d.stream), dhid(n * s.dh * 8, d.stream),
         dys(n * s.dm * 8, d.stream);
@@ -585,7 +634,7 @@ MultiExpertGrads multi_expert_backward(const Matrix& d_ys, const std::vector<For
   for (auto& eg : g.experts) eg = ExpertGrads{Matrix(s.dm, s.dh), Matrix(1, s.dh), Matrix(s.dh, s.dm), Matrix(1, s.dm)};
   if (E == 0) return g;
   auto& d = local();
-  DevPool P = device_pool(experts, s, d.stream);
+  const DevPool& P = device_pool_cached(experts, s, d);
   DevBlocks B = device_blocks(counts, off, d.stream);
   Buf dx = upload(xs, d.stream), dpre = upload(pre, d.stream), dhid = upload(hid, d.stream),
       ddy = upload(d_ys, d.stream), ddx(n * s.dm * 8, d.stream);

@@ -467,11 +467,15 @@ def test_permutes_full_size_round_trips(fm):
 
 
 # --------------------------------------------------------- fp32 layer (§8c)
-def test_layer_f32_vs_oracle(fm, orc):
-    """FMOE_F32 (SIMT fp32) against the oracle fed the same fp32 values:
-    outputs max-abs-err <= 1e-5 * max|ref|, gradients rel-L2 <= 1e-4 (SURVEY
-    §8c parity protocol (3)), routing exact on well-separated tokens."""
-    n, d, h, e, k, seed = 512, 64, 128, 8, 2, 21
+@pytest.mark.parametrize("n,d,h,e,k,seed", [(512, 64, 128, 8, 2, 21),      # 128-row blocks, single CTAs
+                                             (4096, 128, 320, 8, 2, 22),   # 256-row blocks, CTA pairs, h % 256 != 0
+                                             (1000, 192, 256, 16, 3, 23)])  # ragged experts, k = 3
+def test_layer_f32_vs_oracle(fm, orc, n, d, h, e, k, seed):
+    """FMOE_F32 against the oracle fed the same fp32 values: outputs
+    max-abs-err <= 1e-5 * max|ref|, gradients rel-L2 <= 1e-4 (SURVEY §8c
+    parity protocol (3)), routing exact on well-separated tokens.  The expert
+    GEMMs run on the tensor cores (bf16x3 split products, f32x.cu) over
+    aligned expert blocks; the gate stays on the SIMT fp32 kernels."""
     layer = fm.MoELayer(fm.MoEConfig(n, d, h, k, e, 1, seed), dtype=torch.float32)
     f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)  # noqa: E731
     x = f32(orc.seeded_matrix(seed, 102, n, d))
