@@ -974,6 +974,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
               }
             }
+#ifdef FMOE_TC_F32_NOSTORE  // experiment: drain TMEM but store nothing (mainloop-bound speed)
+            if constexpr (EPI == EPI_F32) continue;
+#endif
             if constexpr (C::F32OUT) {
               if (p.tma_out) {
                 // fp32 staging (rows >= M staged as zeros, clipped by the tensor map):
