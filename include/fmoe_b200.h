@@ -202,6 +202,10 @@ int fmoe_softmax_rows(fmoe_ctx* ctx, fmoe_dtype dtype, const void* a, int64_t ro
 int fmoe_topk_rows(fmoe_ctx* ctx, fmoe_dtype dtype, const void* a, int64_t rows, int64_t cols,
                    int64_t k, int32_t* idx, void* vals);
 
+/* dst[i] = src[i] converted between dtypes (round to nearest even), on the
+ * context's stream; n elements. */
+int fmoe_cast(fmoe_ctx* ctx, fmoe_dtype from, const void* src, fmoe_dtype to, void* dst, int64_t n);
+
 /* --------------------------------------------------------- MoE layer (L3) */
 /* One rank's slice of the layer (moe_layer.hpp:17-38): config, replicated
  * gate, local experts g = rank*n_e_local + slot, device weights, gradients and
@@ -225,6 +229,16 @@ int fmoe_layer_grads(fmoe_layer* layer, void** d_wg, fmoe_expert_grads* experts)
 /* Activations kept for backward (MoEForwardCache, moe_layer.hpp:42-50). */
 int fmoe_layer_routing(fmoe_layer* layer, const int32_t** topk_idx, const void** topk_scores,
                        const void** scores, fmoe_plan* plan);
+
+/* Keep the expert pre-activations x*w1 + b1 of each forward
+ * (ForwardCache::preact, expert.hpp:31-35) -- FMOE_F64 / FMOE_F32 layers only
+ * (the bf16 path applies relu in the fc1 epilogue); ShapeError otherwise. */
+int fmoe_layer_keep_preact(fmoe_layer* layer, int keep);
+/* Device pointers of the forward's expert-side activations, in the plan's
+ * layout (rows of expert g at plan offsets): xs = scattered inputs, hidden =
+ * relu(preact), preact (NULL unless kept), ys = expert outputs.  Layer dtype. */
+int fmoe_layer_activations(fmoe_layer* layer, const void** xs, const void** hidden, const void** preact,
+                           const void** ys);
 
 /* forward (moe_layer.cpp:67-110): x [n_b, d_m] -> y [n_b, d_m], dtype. */
 int fmoe_layer_fwd(fmoe_layer* layer, const void* x, void* y);

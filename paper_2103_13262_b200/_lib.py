@@ -84,7 +84,8 @@ EXPORTS = [
     "fmoe_layer_fwd_routed", "fmoe_layer_routing_grad", "fmoe_layer_set_ep_exchange",
     "fmoe_layer_ep_exchange_fused", "fmoe_ep_routes", "fmoe_layer_peer_blob", "fmoe_layer_peer_connect",
     "fmoe_checkpoint_info", "fmoe_layer_load_checkpoint", "fmoe_layer_save_checkpoint",
-    "fmoe_layer_step_host_async", "fmoe_layer_step_host_wait",
+    "fmoe_layer_step_host_async", "fmoe_layer_step_host_wait", "fmoe_cast", "fmoe_layer_keep_preact",
+    "fmoe_layer_activations",
 ]
 
 
@@ -148,6 +149,9 @@ def _load():
         "fmoe_layer_save_checkpoint": [vp, C.c_char_p],
         "fmoe_ep_routes": [C.c_int, C.c_int, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp],
         "fmoe_layer_ep_exchange_fused": [vp, C.POINTER(C.c_int)],
+        "fmoe_cast": [vp, C.c_int, vp, C.c_int, vp, i64],
+        "fmoe_layer_keep_preact": [vp, C.c_int],
+        "fmoe_layer_activations": [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)],
         "fmoe_world_create": [C.c_int, C.POINTER(vp)],
         "fmoe_world_destroy": [vp],
         "fmoe_ctx_join_world": [vp, vp, C.c_int],

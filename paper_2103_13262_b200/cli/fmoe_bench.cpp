@@ -282,6 +282,17 @@ int bench_local_reference_api(const Opts& o) {
       fmoe::backward(d_y, cache, state);
     });
     row(csv.out(), "moe_batched_fwdbwd", o, n_e, 1, both, flops_fwd(o, n_e) + flops_bwd(o, n_e));
+    // the same step with y and d_x read on the host (device-backed results
+    // are copied down on first access): what a caller that consumes them pays
+    double sum = 0.0;
+    const Timing host = measure_host(o.warmup, o.reps, [&] {
+      fmoe::MoEForwardCache cache;
+      const fmoe::Matrix y = fmoe::forward(x, state, nullptr, &cache);
+      const fmoe::Matrix dx = fmoe::backward(d_y, cache, state).first;
+      sum += y.data()[0] + dx.data()[0];
+    });
+    row(csv.out(), "moe_batched_fwdbwd_host_results", o, n_e, 1, host, flops_fwd(o, n_e) + flops_bwd(o, n_e));
+    if (sum != sum) std::cerr << "nan\n";
   }
   return 0;
 }

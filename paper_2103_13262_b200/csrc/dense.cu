@@ -5,6 +5,7 @@
 // topk_rows with the same bits gate_forward produces: they run the very
 // kernels the FMOE_F64 / FMOE_F32 gate uses (gemm_simt.cu, gate.cu).
 #include <string>
+#include <type_traits>
 
 #include "gemm_simt.cuh"
 #include "ops.cuh"
@@ -28,6 +29,20 @@ using namespace fmoe_b200;
   }
 
 namespace {
+template <typename S, typename D>
+__global__ void cast_kernel(const S* __restrict__ src, D* __restrict__ dst, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if constexpr (std::is_same<D, __nv_bfloat16>::value && std::is_same<S, double>::value)
+      dst[i] = __double2bfloat16(src[i]);  // one rounding
+    else if constexpr (std::is_same<D, __nv_bfloat16>::value)
+      dst[i] = __float2bfloat16_rn((float)to_f(src[i]));
+    else if constexpr (std::is_same<S, __nv_bfloat16>::value)
+      dst[i] = (D)__bfloat162float(src[i]);
+    else
+      dst[i] = (D)src[i];  // f64 -> f32 rounds to nearest even, f32 -> f64 exact
+  }
+}
+
 Ctx* CD(fmoe_ctx* c) {
   if (!c) shape_error("null context");
   return reinterpret_cast<Ctx*>(c);
@@ -104,6 +119,23 @@ int fmoe_experts_bwd_cached(fmoe_ctx* ctx, fmoe_dtype dtype, const fmoe_plan* bl
     uint8_t* ws = (uint8_t*)ctx_workspace(x, pre_bytes + 256);
     experts_bwd(x, dtype, *blocks, d_m, d_h, params, xs, hidden, d_ys, d_xs, grads, ws, nullptr, nullptr,
                 preact);
+  })
+}
+
+int fmoe_cast(fmoe_ctx* ctx, fmoe_dtype from, const void* src, fmoe_dtype to, void* dst, int64_t n) {
+  FMOE_GUARD({
+    Ctx* x = CD(ctx);
+    if (n < 0) shape_error("cast: negative size");
+    if (n == 0) return FMOE_OK;
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 16);
+    dispatch_dtype(from, [&](auto* ts) {
+      using S = std::remove_pointer_t<decltype(ts)>;
+      dispatch_dtype(to, [&](auto* td) {
+        using D = std::remove_pointer_t<decltype(td)>;
+        cast_kernel<S, D><<<grid, 256, 0, x->stream>>>((const S*)src, (D*)dst, n);
+      });
+    });
+    CK_LAUNCH(x);
   })
 }
 

@@ -129,6 +129,17 @@ Layer::~Layer() {
   if (h_stage) cudaFreeHost(h_stage);
 }
 
+void Layer::set_keep_preact(bool keep) {
+  if (!keep) {
+    preact_kept = false;
+    return;
+  }
+  if (t == FMOE_BF16) shape_error("keep_preact: the bf16 layer applies relu in the fc1 epilogue");
+  if (cfg.world_size > 1) shape_error("keep_preact: single-worker layers only");
+  if (!preact) preact = dalloc_bytes(owned, plan.capacity * cfg.d_h * es);
+  preact_kept = true;
+}
+
 F32Planes Layer::planes_view() const {
   if (!f32_planes) return F32Planes{};
   return f32_planes_at(f32_planes, cfg.n_b, cfg.d_m, cfg.d_h, E, cfg.n_e_local, plan.capacity);
@@ -226,8 +237,8 @@ void Layer::dispatch_and_experts(const void* x, void* y) {
   scatter(ctx, t, x, d, plan, xs);                                // dispatch.cpp:49-59
   ctx_mark(ctx, MARK_SCATTER);
   const F32Planes pv = planes_view();
-  experts_fwd(ctx, t, plan, d, h, params(), xs, hidden, ys, relu_bits, nullptr, nullptr, nullptr,
-              f32_planes ? &pv : nullptr);  // expert.cpp:85-102
+  experts_fwd(ctx, t, plan, d, h, params(), xs, hidden, ys, relu_bits, preact_kept ? preact : nullptr, nullptr,
+              nullptr, f32_planes ? &pv : nullptr);  // expert.cpp:85-102
   gather_combine(ctx, t, ys, d, plan, vals, y);                   // dispatch.cpp:61-78
   ctx_mark(ctx, MARK_GATHER);
   fwd_done = true;

@@ -24,6 +24,8 @@ struct Layer {
   int32_t* idx = nullptr;
   fmoe_plan plan{};
   void *xs = nullptr, *hidden = nullptr, *ys = nullptr;
+  void* preact = nullptr;  // x*w1 + b1, when kept (fmoe_layer_keep_preact; SIMT / F32 dtypes)
+  bool preact_kept = false;
   bool fwd_done = false;
   bool routed = false;
   int prof_slot = -1;   // profiling slot of the current forward (Prof)  // forward_routed: routing injected, no gate on this step
@@ -61,6 +63,7 @@ struct Layer {
   fmoe_expert_params params() const;
   fmoe_expert_grads grads() const;
   void init_weights();
+  void set_keep_preact(bool keep);
   void forward(const void* x, void* y);
   void forward_routed(const void* x, const int32_t* topk_idx, const void* topk_scores, void* y);
   void dispatch_and_experts(const void* x, void* y);

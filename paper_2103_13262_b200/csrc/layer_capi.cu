@@ -42,6 +42,19 @@ int fmoe_layer_params(fmoe_layer* layer, void** w_g, fmoe_expert_params* experts
   })
 }
 
+int fmoe_layer_keep_preact(fmoe_layer* layer, int keep) { FMOE_GUARD(L(layer)->set_keep_preact(keep != 0)) }
+
+int fmoe_layer_activations(fmoe_layer* layer, const void** xs, const void** hidden, const void** preact,
+                           const void** ys) {
+  FMOE_GUARD({
+    Layer* l = L(layer);
+    if (xs) *xs = l->xs;
+    if (hidden) *hidden = l->hidden;
+    if (preact) *preact = l->preact;
+    if (ys) *ys = l->ys;
+  })
+}
+
 int fmoe_layer_grads(fmoe_layer* layer, void** d_wg, fmoe_expert_grads* experts) {
   FMOE_GUARD({
     Layer* l = L(layer);

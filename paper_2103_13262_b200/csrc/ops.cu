@@ -284,7 +284,7 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
                  const Arrival* arrive, const F32Planes* planes) {
   const int64_t E = b.n_experts;
   if (E == 0) return;
-  if (t == FMOE_F32 && phase == EXPERTS_BWD_ALL && !dxs_route && f32_tc_route(b, d, h)) {
+  if (t == FMOE_F32 && phase == EXPERTS_BWD_ALL && !dxs_route && part_ws && f32_tc_route(b, d, h)) {
     // tensor cores, bf16x3 (f32x.cu); group order after the bias partials
     int* order = reinterpret_cast<int*>(part_ws + (b.capacity / 128 + 1) * (d + h));
     experts_bwd_f32tc(ctx, b, d, h, w, xs, hidden, d_ys, d_xs, g, d_pre, mask, order, planes);

@@ -188,7 +188,7 @@ Matrix allreduce_sum(const Matrix& m, std::span<const int> group, Transport& tra
   if (group.empty()) throw ProtocolError("allreduce_sum: empty group");
   Matrix out = m;
   cudaStream_t s = t.stream();
-  Buf b = dropin::upload(m, s);
+  Buf b = dropin::upload_copy(m, s);  // reduced in place: a private copy
   check(fmoe_allreduce_sum(t.device_context(), FMOE_F64, b.get(), (int64_t)m.size(), group.data(),
                            (int64_t)group.size()));
   if (out.size()) dropin::cuda(cudaMemcpyAsync(out.data(), b.get(), out.size() * 8, cudaMemcpyDeviceToHost, s), "D2H");
@@ -281,6 +281,8 @@ Matrix forward(const Matrix& x, const MoELayerState& state, Transport* transport
     throw ProtocolError("forward: transport world != config world");
   if (!ep && state.experts.size() != c.total_experts())
     throw ShapeError("forward: single-worker call needs all experts local");
+  if (!ep)
+    if (auto y = dropin::fast_forward(x, state, cache)) return std::move(*y);  // device-resident route (fast.cpp)
 
   GateOutput gate_out = gate_forward(x, state.gate, c.k);
   DispatchPlan plan = build_plan(gate_out.topk_indices, c.total_experts());
@@ -316,6 +318,8 @@ std::pair<Matrix, MoEGrads> backward(const Matrix& d_y, const MoEForwardCache& c
                                      Transport* transport) {
   const bool ep = cache.exchange.has_value();
   if (ep && !transport) throw ProtocolError("backward: cache came from a distributed forward, transport required");
+  if (!ep)
+    if (auto r = dropin::fast_backward(d_y, cache, state)) return std::move(*r);  // device-resident route
   GatherCombineGrads comb = gather_combine_backward(d_y, cache.expert_outputs, cache.plan, cache.gate_out.topk_scores);
   MoEGrads grads;
   Matrix d_xs;
@@ -337,6 +341,8 @@ std::pair<Matrix, MoEGrads> backward(const Matrix& d_y, const MoEForwardCache& c
 }
 
 double train_step(const Matrix& x, const Matrix& target, MoELayerState& state, double lr, Transport* transport) {
+  if (!(transport && state.config.world_size > 1) && state.experts.size() == state.config.total_experts())
+    if (auto loss = dropin::fast_train_step(x, target, state, lr)) return *loss;  // one device step (fast.cpp)
   MoEForwardCache cache;
   const Matrix y = forward(x, state, transport, &cache);
   if (!target.same_shape(y)) throw ShapeError("train_step: target shape != output shape");

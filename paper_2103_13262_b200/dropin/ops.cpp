@@ -3,6 +3,8 @@
 // (reference API: proj/include/fmoe/{matrix,rng,gate,dispatch,expert}.hpp).
 #include <atomic>
 #include <cmath>
+#include <cstdio>
+#include <mutex>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -60,17 +62,71 @@ Buf::Buf(std::size_t bytes, cudaStream_t s) : s_(s) {
   cuda(cudaMallocAsync(&p_, bytes < 16 ? 16 : bytes, s), "cudaMallocAsync");
 }
 Buf::~Buf() {
-  if (p_) cudaFreeAsync(p_, s_);
+  if (p_ && owned_) cudaFreeAsync(p_, s_);
 }
-Buf::Buf(Buf&& o) noexcept : p_(o.p_), s_(o.s_) { o.p_ = nullptr; }
+Buf::Buf(Buf&& o) noexcept : p_(o.p_), s_(o.s_), owned_(o.owned_) { o.p_ = nullptr; }
 Buf& Buf::operator=(Buf&& o) noexcept {
   if (this != &o) {
-    if (p_) cudaFreeAsync(p_, s_);
+    if (p_ && owned_) cudaFreeAsync(p_, s_);
     p_ = o.p_;
     s_ = o.s_;
+    owned_ = o.owned_;
     o.p_ = nullptr;
   }
   return *this;
+}
+
+Buf upload(const Matrix& m, cudaStream_t s) {
+  if (const auto& st = m.device_store()) return Buf::view(st->f64(m.device_offset()));
+  return upload(m.data(), m.size() * sizeof(double), s);
+}
+
+Buf upload_copy(const Matrix& m, cudaStream_t s) {
+  if (const auto& st = m.device_store()) {
+    Buf b(m.size() * sizeof(double), s);
+    if (m.size())
+      cuda(cudaMemcpyAsync(b.get(), st->f64(m.device_offset()), m.size() * sizeof(double), cudaMemcpyDeviceToDevice,
+                           s),
+           "D2D");
+    return b;
+  }
+  return upload(m.data(), m.size() * sizeof(double), s);
+}
+
+namespace {
+// One stream per device for the stores' pool allocations and frees; the
+// device's default memory pool keeps freed blocks for reuse.
+cudaStream_t pool_stream(int device) {
+  static std::once_flag once[64];
+  static cudaStream_t streams[64];
+  std::call_once(once[device & 63], [device] {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(device);
+    cudaStreamCreateWithFlags(&streams[device & 63], cudaStreamNonBlocking);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      std::uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaSetDevice(cur);
+  });
+  return streams[device & 63];
+}
+}  // namespace
+
+std::shared_ptr<detail::DeviceStore> device_store(std::size_t bytes, const Device& d) {
+  auto st = std::make_shared<detail::DeviceStore>();
+  st->device = d.device;
+  st->bytes = bytes;
+  cudaStream_t ps = pool_stream(d.device);
+  cuda(cudaMallocAsync(&st->ptr, bytes < 16 ? 16 : bytes, ps), "cudaMallocAsync (device store)");
+  cudaEvent_t ev;
+  cuda(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+  cuda(cudaEventRecord(ev, ps), "cudaEventRecord");
+  cuda(cudaStreamWaitEvent(d.stream, ev, 0), "cudaStreamWaitEvent");
+  cudaEventDestroy(ev);
+  return st;
 }
 
 Buf upload(const void* host, std::size_t bytes, cudaStream_t s) {
@@ -107,6 +163,28 @@ std::vector<std::int64_t> download_i32(const Buf& b, std::size_t n, const Device
 std::uint64_t Matrix::next_id() noexcept {
   static std::atomic<std::uint64_t> next{1};
   return next.fetch_add(1, std::memory_order_relaxed);
+}
+
+detail::DeviceStore::~DeviceStore() {
+  if (ptr) cudaFreeAsync(ptr, dropin::pool_stream(device));
+}
+
+// First host access of a device-backed Matrix: copy its values down (the
+// stores are complete: every drop-in call synchronised before returning).
+void Matrix::fetch() const noexcept {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (host_ok_.load(std::memory_order_acquire)) return;
+  data_.resize(rows_ * cols_);
+  if (!data_.empty()) {
+    const cudaError_t e = cudaMemcpy(data_.data(), dev_->f64(dev_off_), data_.size() * sizeof(double),
+                                     cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+      std::fprintf(stderr, "fmoe drop-in: device -> host copy of a result failed: %s\n", cudaGetErrorString(e));
+      std::abort();
+    }
+  }
+  host_ok_.store(true, std::memory_order_release);
 }
 
 using dropin::Buf;
@@ -491,18 +569,27 @@ struct DevPool {
 };
 DevPool device_pool(std::span<const ExpertParams> experts, const Shapes& s, cudaStream_t st) {
   const std::size_t E = experts.size();
-  std::vector<double> w1(E * s.dm * s.dh), b1(E * s.dh), w2(E * s.dh * s.dm), b2(E * s.dm);
-  for (std::size_t e = 0; e < E; ++e) {
-    std::memcpy(w1.data() + e * s.dm * s.dh, experts[e].w1.data(), s.dm * s.dh * 8);
-    std::memcpy(b1.data() + e * s.dh, experts[e].b1.data(), s.dh * 8);
-    std::memcpy(w2.data() + e * s.dh * s.dm, experts[e].w2.data(), s.dh * s.dm * 8);
-    std::memcpy(b2.data() + e * s.dm, experts[e].b2.data(), s.dm * 8);
-  }
   DevPool P;
-  P.w1 = upload(w1.data(), w1.size() * 8, st);
-  P.b1 = upload(b1.data(), b1.size() * 8, st);
-  P.w2 = upload(w2.data(), w2.size() * 8, st);
-  P.b2 = upload(b2.data(), b2.size() * 8, st);
+  P.w1 = Buf(E * s.dm * s.dh * 8, st);
+  P.b1 = Buf(E * s.dh * 8, st);
+  P.w2 = Buf(E * s.dh * s.dm * 8, st);
+  P.b2 = Buf(E * s.dm * 8, st);
+  // stacked [E, ...] copies: device-to-device for device-backed parameters
+  // (after train_step), from the host values otherwise
+  auto put = [&](const Matrix& m, Buf& b, std::size_t e, std::size_t n) {
+    double* dst = b.as<double>() + e * n;
+    if (const auto& ds = m.device_store())
+      dropin::cuda(cudaMemcpyAsync(dst, ds->f64(m.device_offset()), n * 8, cudaMemcpyDeviceToDevice, st), "D2D");
+    else if (n)
+      dropin::cuda(cudaMemcpyAsync(dst, m.data(), n * 8, cudaMemcpyHostToDevice, st), "H2D");
+  };
+  for (std::size_t e = 0; e < E; ++e) {
+    put(experts[e].w1, P.w1, e, s.dm * s.dh);
+    put(experts[e].b1, P.b1, e, s.dh);
+    put(experts[e].w2, P.w2, e, s.dh * s.dm);
+    put(experts[e].b2, P.b2, e, s.dm);
+  }
+  dropin::cuda(cudaStreamSynchronize(st), "H2D sync");
   P.p = {P.w1.get(), P.b1.get(), P.w2.get(), P.b2.get()};
   return P;
 }
