@@ -236,6 +236,35 @@ def cpu_reference(n_tokens: int, cfg: dict, min_seconds: float = 10.0, max_reps:
                        f"FMOE_THREADS={cores}, built {build}")}
 
 
+def reference_api_line(cfg: dict, reps: int = 5):
+    """tokens/s of fmoe::forward + fmoe::backward (the reference's C++ API)
+    through libfmoe_dropin.so, FMOE_F64, via fmoe_bench bench-local --api
+    reference (the reference's moe_batched_fwdbwd loop)."""
+    exe = os.path.join(ROOT, "paper_2103_13262_b200", "fmoe_bench")
+    if not os.path.exists(exe):
+        return {"unavailable": "paper_2103_13262_b200/fmoe_bench not built"}
+    cmd = [exe, "bench-local", "--api", "reference", "--n-b", str(cfg["n_b"]), "--d-m", str(cfg["d_m"]),
+           "--d-h", str(cfg["d_h"]), "--k", str(cfg["k"]), "--n-e", str(cfg["n_e_local"]), "--reps", str(reps),
+           "--warmup", "2"]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=600).stdout
+    except Exception as e:  # report, never guess
+        return {"unavailable": f"fmoe_bench failed: {e}"}
+    rows = {r.split(",")[0]: r.split(",") for r in out.splitlines() if r and not r.startswith(("#", "scenario"))}
+    if "moe_batched_fwdbwd" not in rows:
+        return {"unavailable": "fmoe_bench printed no moe_batched_fwdbwd row: " + out[-300:]}
+    ms = float(rows["moe_batched_fwdbwd"][8])
+    ms_host = float(rows["moe_batched_fwdbwd_host_results"][8]) if "moe_batched_fwdbwd_host_results" in rows else None
+    return {"value": cfg["n_b"] / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+            "value_host_results": cfg["n_b"] / (ms_host / 1e3) if ms_host else None, "ms_per_step_host_results": ms_host,
+            "dtype": "f64 (FMOE_F64: bit-identical to the reference and to the drop-in's operator composition)",
+            "path": ("fmoe::init_state / forward(x, state, nullptr, &cache) / backward(d_y, cache, state) of the "
+                     "reference headers (include/fmoe/moe_layer.hpp) through libfmoe_dropin.so's device-resident "
+                     "route: x, d_y uploaded per step, parameters resident, results device-backed Matrices"),
+            "value_host_results_note": "the same loop with y and d_x read on the host every step",
+            "timing": f"host steady_clock, warm-up 2 + {reps} reps (fmoe_bench bench-local --api reference)"}
+
+
 def cpu_tokens_for(cores: int) -> int:
     return max(256, min(4096, 64 * cores))
 
@@ -561,6 +590,14 @@ def run_ours(args, world, rank, cfg):
                                               "step (copy stream, double-buffered), d_y device-resident, d_x left "
                                               "on the device, one fp32 scalar (sum of y) read back per step")}}
 
+    # cfg1: the same workload through the reference's own C++ API (fmoe::forward
+    # + fmoe::backward of include/fmoe/moe_layer.hpp, host Matrix values) served
+    # by libfmoe_dropin.so on this GPU in FMOE_F64 -- bit-identical to the
+    # reference -- timed by the reference's bench-local loop (host clock)
+    ref_api = None
+    if wl == "cfg1" and rank == 0:
+        ref_api = reference_api_line(cfg)
+
     pk = peaks()
     peak, peak_why = tensor_peak(pk, clk)
     # expert GEMM FLOPs of one launch (fmoe_bench.cpp:110-126): 2 * rows * d * h,
@@ -635,6 +672,8 @@ def run_ours(args, world, rank, cfg):
     }
     if e2e is not None:
         line["e2e"] = e2e
+    if ref_api is not None:
+        line["reference_api"] = ref_api
     if world > 1:
         fused = bool(getattr(layer0, "ep_exchange_fused", False))
         st = stage_ms
