@@ -4,8 +4,10 @@
 // parameters they leave.  tests/test_dropin.py runs it on the device-resident
 // route (default) and on the operator composition (FMOE_DROPIN_PATH=ops) and
 // compares the dumps.
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "fmoe/moe_layer.hpp"
@@ -20,6 +22,22 @@ static void dump(std::FILE* f, const Matrix& m) {
   std::fwrite(m.data(), sizeof(double), m.size(), f);
 }
 
+// FAST_ROUTE_ROUND_BF16=1: inputs and weight matrices rounded to bf16 values
+// (round to nearest even through fp32), biases to fp32 -- the values the bf16
+// layer stores -- so both runs of the reduced-precision comparison start from
+// the same numbers (the oracle is fed the rounded values)
+static double round_bf16(double v) {
+  float f = (float)v;
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+static void round_matrix(Matrix& m, bool to_bf16) {
+  for (std::size_t i = 0; i < m.size(); ++i) m.data()[i] = to_bf16 ? round_bf16(m.data()[i]) : (double)(float)m.data()[i];
+}
+
 int main(int argc, char** argv) {
   if (argc < 2) return 2;
   const std::size_t n = argc > 2 ? std::atoi(argv[2]) : 512, d = argc > 3 ? std::atoi(argv[3]) : 128,
@@ -30,6 +48,15 @@ int main(int argc, char** argv) {
   UniformRng(stream_seed(7, 102)).fill(x, -1.0, 1.0);
   UniformRng(stream_seed(7, 103)).fill(dy, -1.0, 1.0);
   UniformRng(stream_seed(7, 104)).fill(tgt, -1.0, 1.0);
+  if (const char* r = std::getenv("FAST_ROUTE_ROUND_BF16"); r && *r == '1') {
+    for (Matrix* m : {&x, &dy, &tgt, &st.gate.w_g}) round_matrix(*m, true);
+    for (auto& p : st.experts) {
+      round_matrix(p.w1, true);
+      round_matrix(p.w2, true);
+      round_matrix(p.b1, false);
+      round_matrix(p.b2, false);
+    }
+  }
   std::FILE* f = std::fopen(argv[1], "wb");
   MoEForwardCache cache;
   const Matrix y = forward(x, st, nullptr, &cache);

@@ -122,20 +122,20 @@ def test_dropin_device_route_reduced_precision(tmp_path, dtype):
     reference API on the tensor cores.  f32: every section (y, the whole
     cache, d_x, all gradients, losses, trained parameters, last forward)
     within SURVEY 8(c)'s fp32 gradient bound (rel-L2 1e-4) of the f64
-    composition.  bf16: the route rounds the caller's f64 inputs and weights
-    to bf16 while the reference keeps them (8(c)'s bf16 rule compares against
-    an oracle fed the ROUNDED values, tests/test_gpu_fullsize.py), and a
-    near-tie token may take another expert -- so y is compared on the tokens
-    whose top-k matches at 1e-2, d_x (through the gate's softmax Jacobian,
-    which amplifies the input rounding) and the gradients, losses and trained
-    parameters at 5e-2, the cache sections not at all (rerouting shifts
-    rows)."""
+    composition.  bf16: SURVEY 8(c)'s bf16 rule compares against the oracle
+    fed the ROUNDED values, so both runs start from inputs and weights rounded
+    to bf16 (biases to fp32; FAST_ROUTE_ROUND_BF16=1) and the remaining
+    difference is the route's bf16 storage of activations with fp32
+    accumulation: y and d_x on the tokens whose top-k matches at 1e-2 / 2e-2,
+    the gradients, losses and trained parameters at 2e-2, the cache sections
+    not at all (a rerouted near-tie token shifts rows)."""
     import numpy as np
 
     E, k, n, d = 8, 2, 1024, 128
     shape = (str(n), str(d), "256", str(E))
-    _, low = _fast_route_dump(tmp_path, dtype, {"FMOE_DROPIN_DTYPE": dtype}, shape)
-    _, ref = _fast_route_dump(tmp_path, "ops", {"FMOE_DROPIN_PATH": "ops"}, shape)
+    rnd = {"FAST_ROUTE_ROUND_BF16": "1"} if dtype == "bf16" else {}
+    _, low = _fast_route_dump(tmp_path, dtype, {"FMOE_DROPIN_DTYPE": dtype, **rnd}, shape)
+    _, ref = _fast_route_dump(tmp_path, "ops", {"FMOE_DROPIN_PATH": "ops", **rnd}, shape)
     n_cache = 4 + 3 * E
     assert len(low) == len(ref) == n_cache + 2 + 4 * E + 2 + 3 + 1 + 4 * E + 1
     rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))  # noqa: E731
@@ -147,10 +147,10 @@ def test_dropin_device_route_reduced_precision(tmp_path, dtype):
         return
     top = lambda s: np.sort(np.argsort(-s.reshape(n, E), axis=1, kind="stable")[:, :k], axis=1)  # noqa: E731
     same = (top(low[1]) == top(ref[1])).all(axis=1)
-    assert same.mean() > 0.95, same.mean()
+    assert same.mean() > 0.99, same.mean()
     rows = lambda s: s.reshape(n, d)[same]  # noqa: E731
     assert rel(rows(low[0]), rows(ref[0])) < 1e-2                      # y
-    assert rel(rows(low[n_cache]), rows(ref[n_cache])) < 5e-2          # d_x
+    assert rel(rows(low[n_cache]), rows(ref[n_cache])) < 2e-2          # d_x
     for i in range(n_cache + 1, len(ref)):
         if i in (n_cache + 1 + 4 * E, n_cache + 2 + 4 * E):           # edited-cache d_x, d_wg (f64 composition)
             continue
@@ -159,4 +159,4 @@ def test_dropin_device_route_reduced_precision(tmp_path, dtype):
         if i == len(ref) - 1:                                          # last forward: matched tokens
             assert rel(rows(a), rows(b)) < 2e-2
         elif b.size and np.linalg.norm(b):
-            assert rel(a, b) < 5e-2, (i, rel(a, b))
+            assert rel(a, b) < 2e-2, (i, rel(a, b))
