@@ -337,7 +337,7 @@ def run_reference(args, world, rank, cfg):
 def workload_name(workload, cfg, world):
     if workload == "cfg1":
         return ("cfg1: single MoE layer d_model=1024 d_hidden=4096, 16 experts top-2, 8192 tokens, fp32 "
-                "(FMOE_F32: gate and permutes in fp32, expert GEMMs as bf16x3 split products on the tensor "
+                "(FMOE_F32: gate and permutes in fp32, expert GEMMs as bf16x6 split products on the tensor "
                 "cores, fp32 accumulate), fwd+bwd")
     if workload == "cfg2":
         if world == 1:
@@ -607,10 +607,10 @@ def run_ours(args, world, rank, cfg):
     avg_launch_ms = sum(gemm_ms) / len(gemm_ms)
     if avg_launch_ms <= 0:  # no per-GEMM stage marks on this path (FMOE_F32_SIMT)
         avg_launch_ms = float("nan")
-    # cfg1 (FMOE_F32): each expert GEMM is 3 bf16 passes on the tensor pipe
-    # (bf16x3 split products, f32x.cu); the roofline counts the pipe's work,
-    # algorithmic_fp32_tflops the fp32 FLOPs the layer delivers
-    passes = 3 if wl == "cfg1" else 1
+    # cfg1 (FMOE_F32): each expert GEMM is 6 bf16 passes on the tensor pipe
+    # (bf16x6 split products, tc_gemm.cuh / f32x.cu); the roofline counts the
+    # pipe's work, algorithmic_fp32_tflops the fp32 FLOPs the layer delivers
+    passes = 6 if wl == "cfg1" else 1
     achieved = passes * flop_gemm / (avg_launch_ms / 1e3) / 1e12
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -652,10 +652,11 @@ def run_ours(args, world, rank, cfg):
                                          for s_ in GEMM_STAGES if stage_ms[s_] > 0},
                      **({"algorithmic_fp32_tflops": flop_gemm / (avg_launch_ms / 1e3) / 1e12,
                          "bf16_passes_per_gemm": passes,
-                         "note": ("FMOE_F32: fp32 operands split into bf16 hi/lo planes, each GEMM = hi*lo' + lo*hi' + "
-                                  "hi*hi' on tcgen05 into one fp32 accumulator (3 bf16 passes); 'achieved' counts the "
+                         "note": ("FMOE_F32: fp32 operands split into three bf16 planes a0 + a1 + a2, each GEMM = "
+                                  "a0*b2 + a2*b0 + a1*b1 + a0*b1 + a1*b0 + a0*b0 on tcgen05 into one fp32 accumulator "
+                                  "(6 bf16 passes); 'achieved' counts the "
                                   "tensor pipe's bf16 work, per_gemm_tflops the fp32 FLOPs; stage times include the "
-                                  "hi/lo split passes of the stage's operands")} if passes > 1 else {}),
+                                  "plane-split passes of the stage's operands")} if passes > 1 else {}),
                      **({"note": ("averaged over the six expert GEMMs; with few rows per expert the weight-gradient "
                                   "launches are bound by writing fp32 gradients (HBM), not by the tensor pipe "
                                   "(profiles/r01h_cfg4_wgrad.md); fc1/fc2/dgrad stages in stages_ms")}

@@ -5,6 +5,7 @@
 // (tc_gemm.cu): operands are used in their stored layouts through K-major or
 // MN-major TMA descriptors, so no transpose is ever materialised.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "gemm_simt.cuh"
@@ -103,6 +104,7 @@ void gate_fwd(Ctx* ctx, fmoe_dtype t, const void* x, const void* wg, int64_t n, 
     p.topk_idx = idx;
     p.topk_val = (float*)vals;
     p.topk = k <= 8 ? (int)k : 0;
+    p.row_split = 1;  // balanced row ranges per SM (tc_gemm.cuh)
     const int bn = pick_bn(e);
     tc::launch(ctx, bn, false, true, ta, tb, p, ceil_div(n, 128));
     if (k > 8) gate_softmax_topk(ctx, FMOE_F32, nullptr, n, e, k, scores, idx, vals, true);
@@ -381,7 +383,8 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
   float* part_b2 = part_ws + t128 * h;
   if (do_wgrad) {
     tile_colsum(ctx, (const __nv_bfloat16*)d_ys, d, b.n_tiles, t128, part_b2);
-    reduce_tile_partials(ctx, part_b2, d, b.offsets, E, (float*)g.d_b2);
+    // d_b1's partials (dgrad-fc2 epilogue) are complete here too: one reduce launch for both
+    reduce_tile_partials(ctx, part_b2, d, b.offsets, E, (float*)g.d_b2, part_ws, h, (float*)g.d_b1);
     ctx_mark(ctx, MARK_DB2);
   }
   if (do_dgrad) {  // dgrad fc1: d_xs = d_pre W1^T; B(k=j, n=c) = W1[e][c][j] -> K-major [E*d, h]
@@ -407,10 +410,7 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     tc::launch(ctx, 256, true, true, ta, tb, p, E * ceil_div(d, 128 * cg) * ceil_div(h, 256), cg);
     ctx_mark(ctx, MARK_WGRAD1);
   }
-  if (do_wgrad) {  // d_b1 partials come from the dgrad-fc2 epilogue
-    reduce_tile_partials(ctx, part_ws, h, b.offsets, E, (float*)g.d_b1);
-    ctx_mark(ctx, MARK_DB1);
-  }
+  if (do_wgrad) ctx_mark(ctx, MARK_DB1);  // d_b1 was reduced with d_b2 above
 }
 
 int64_t experts_bwd_part_floats(const fmoe_plan& b, int64_t d, int64_t h) {

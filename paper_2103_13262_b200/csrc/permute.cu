@@ -521,16 +521,32 @@ __global__ void __launch_bounds__(256) tile_colsum_kernel(const __nv_bfloat16* _
   }
 }
 
-// out[e][c] = sum over expert e's tiles, in tile order (deterministic).
-__global__ void reduce_tile_partials_kernel(const float* __restrict__ part, int64_t n_cols,
-                                            const int32_t* __restrict__ offsets, float* __restrict__ out) {
+// out[e][c] = sum over expert e's tiles, in tile order (deterministic).  Two
+// partial sets in one launch: column blocks [0, nb1) reduce part1 (n1
+// columns), the rest part2 (n2 columns); eight tiles' loads in flight.
+__global__ void reduce_tile_partials_kernel(const float* __restrict__ part1, int64_t n1, float* __restrict__ out1,
+                                            const float* __restrict__ part2, int64_t n2, float* __restrict__ out2,
+                                            const int32_t* __restrict__ offsets) {
   const int e = blockIdx.y;
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n_cols) return;
+  const int64_t nb1 = (n1 + blockDim.x - 1) / blockDim.x;
+  const bool first = blockIdx.x < nb1;
+  const float* part = first ? part1 : part2;
+  const int64_t n = first ? n1 : n2;
+  float* out = first ? out1 : out2;
+  const int64_t c = (int64_t)(first ? blockIdx.x : blockIdx.x - nb1) * blockDim.x + threadIdx.x;
+  if (c >= n) return;
   const int t0 = __ldg(offsets + e) / 128, t1 = __ldg(offsets + e + 1) / 128;
   float s = 0.f;
-  for (int t = t0; t < t1; ++t) s += part[(int64_t)t * n_cols + c];
-  out[(int64_t)e * n_cols + c] = s;
+  int t = t0;
+  for (; t + 8 <= t1; t += 8) {
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = part[(int64_t)(t + j) * n + c];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += v[j];
+  }
+  for (; t < t1; ++t) s += part[(int64_t)t * n + c];
+  out[(int64_t)e * n + c] = s;
 }
 
 // order[rank] = group, ranked by decreasing row count (offsets[g+1] -
@@ -565,10 +581,11 @@ void tile_colsum(Ctx* ctx, const __nv_bfloat16* src, int64_t n_cols, const int32
 }
 
 void reduce_tile_partials(Ctx* ctx, const float* part, int64_t n_cols, const int32_t* offsets,
-                          int64_t n_blocks, float* out) {
-  if (n_blocks == 0 || n_cols == 0) return;
-  dim3 grid((unsigned)ceil_div(n_cols, 256), (unsigned)n_blocks);
-  reduce_tile_partials_kernel<<<grid, 256, 0, ctx->stream>>>(part, n_cols, offsets, out);
+                          int64_t n_blocks, float* out, const float* part2, int64_t n_cols2, float* out2) {
+  if (n_blocks == 0 || (n_cols == 0 && n_cols2 == 0)) return;
+  if (!part2) n_cols2 = 0;
+  dim3 grid((unsigned)(ceil_div(n_cols, 256) + ceil_div(n_cols2, 256)), (unsigned)n_blocks);
+  reduce_tile_partials_kernel<<<grid, 256, 0, ctx->stream>>>(part, n_cols, out, part2, n_cols2, out2, offsets);
   CK_LAUNCH(ctx);
 }
 

@@ -36,8 +36,10 @@ void block_colsum(Ctx* ctx, fmoe_dtype t, const void* src, int64_t n_cols, const
 // part[t][c] = sum of tile t's rows; out[e][c] = sum of expert e's tile partials.
 void tile_colsum(Ctx* ctx, const __nv_bfloat16* src, int64_t n_cols, const int32_t* n_tiles,
                  int64_t max_tiles, float* part);
+// (part2 / n_cols2 / out2: a second partial set over the same tiles, same launch)
 void reduce_tile_partials(Ctx* ctx, const float* part, int64_t n_cols, const int32_t* offsets,
-                          int64_t n_blocks, float* out);
+                          int64_t n_blocks, float* out, const float* part2 = nullptr, int64_t n_cols2 = 0,
+                          float* out2 = nullptr);
 
 // gate (gate.cu)
 void gate_softmax_topk(Ctx* ctx, fmoe_dtype t, const void* logits, int64_t n, int64_t e, int64_t k,

@@ -87,6 +87,15 @@ __device__ __forceinline__ void tma_store_commit_warp(const CUtensorMap* m, uint
       "r"(src), "r"(c0), "r"(c1)
       : "memory");
 }
+// One thread's 1-D bulk copy shared -> global (16-byte aligned, bytes % 16 == 0)
+// as its own bulk group; that thread's bulk_wait_read / bulk_wait_all cover it.
+__device__ __forceinline__ void bulk_store_1d(void* gdst, uint32_t ssrc, uint32_t bytes) {
+  asm volatile(
+      "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
+      "cp.async.bulk.commit_group;" ::"l"(reinterpret_cast<uint64_t>(gdst)),
+      "r"(ssrc), "r"(bytes)
+      : "memory");
+}
 // wait until at most N committed groups are still reading shared memory
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {

@@ -39,7 +39,11 @@ struct Cfg {
 #endif
   static constexpr int NBUF = F32OUT ? FMOE_TC_F32_NBUF : FMOE_TC_BF16_NBUF;
   static constexpr int TILE_BYTES = 32 * OUT_ROW_BYTES;
-  static constexpr int STORE_BYTES = TMA_STORE ? 8 * NBUF * TILE_BYTES : 0;
+  // gate (E <= 64): each epilogue lane stages its row of scores (padded to
+  // avoid bank conflicts) and stores it as one contiguous bulk copy
+  static constexpr bool GATE_STAGE = EPI == EPI_GATE && BN == 64;
+  static constexpr int GATE_ROW_BYTES = BN * 4 + 16;
+  static constexpr int STORE_BYTES = TMA_STORE ? 8 * NBUF * TILE_BYTES : GATE_STAGE ? 8 * 32 * GATE_ROW_BYTES : 0;
   // bf16 epilogues stage the bias of each warp's 128-column slice of the tile
   static constexpr int BIAS_BYTES = EPI == EPI_BF16 ? 8 * (BN / 2) * 4 : 0;
 #ifndef FMOE_TC_SMEM_KB
@@ -49,8 +53,8 @@ struct Cfg {
 #ifndef FMOE_TC_F32_SMEM_KB
 #define FMOE_TC_F32_SMEM_KB FMOE_TC_SMEM_KB
 #endif
-  static constexpr int BUDGET =
-      (F32OUT ? FMOE_TC_F32_SMEM_KB : FMOE_TC_SMEM_KB) * 1024 - 1280 /*align + barriers*/ - STORE_BYTES - COLSUM_BYTES - BIAS_BYTES;
+  static constexpr int BUDGET = (GATE_STAGE ? 224 : F32OUT ? FMOE_TC_F32_SMEM_KB : FMOE_TC_SMEM_KB) * 1024 -
+                                1280 /*align + barriers*/ - STORE_BYTES - COLSUM_BYTES - BIAS_BYTES;
   static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
   static constexpr int SMEM =
       STAGES * STAGE_BYTES + STORE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + COLSUM_BYTES + BIAS_BYTES;
@@ -99,6 +103,7 @@ __device__ __forceinline__ constexpr uint32_t idesc() {
 struct Tile {
   int g, m0, n0, kbeg, nkb;  // m0: first row of the (pair) tile; nkb: k-blocks of all phases
   int kpp;                   // k-blocks per phase (bf16x3: nkb = 3 * kpp)
+  int lo, hi;                // RAGGED_M: rows the epilogue owns (row_split chunks overlap)
 };
 
 template <int BN>
@@ -112,6 +117,7 @@ template <int BN, int CG>
 __device__ __forceinline__ int total_tiles(const Params& p) {
   const int nn = n_tiles_n<BN>(p);
   if (p.mode == RAGGED_M) {
+    if (p.row_split) return p.row_split * p.row_chunks;
     const int nm = p.n_mtiles ? (*p.n_mtiles + CG - 1) / CG : (p.M + BM * CG - 1) / (BM * CG);
     return nm * nn;
   }
@@ -122,7 +128,18 @@ template <int BN, int CG, bool SPLIT = false>
 __device__ __forceinline__ Tile decode(const Params& p, int t) {
   Tile r;
   const int nn = n_tiles_n<BN>(p);
-  if (p.mode == RAGGED_M) {
+  if (p.mode == RAGGED_M && p.row_split) {  // balanced row ranges (CG = 1, N <= BN)
+    const int S = p.row_split, slot = t % S, c = t / S;
+    const int rb = (int)((int64_t)slot * p.M / S), re = (int)((int64_t)(slot + 1) * p.M / S);
+    const int start = rb + c * BM;
+    r.m0 = re - rb >= BM ? min(start, re - BM) : rb;
+    r.lo = start;
+    r.hi = min(re, r.m0 + BM);
+    r.n0 = 0;
+    r.g = 0;
+    r.kbeg = 0;
+    r.kpp = start < re ? (p.K + BK - 1) / BK : 0;
+  } else if (p.mode == RAGGED_M) {
     const int mt0 = t / nn;
     r.n0 = (t - mt0 * nn) * BN;
     const int mt = p.mtile_order ? __ldg(p.mtile_order + mt0) : mt0;
@@ -130,6 +147,8 @@ __device__ __forceinline__ Tile decode(const Params& p, int t) {
     r.g = p.tile_group ? __ldg(p.tile_group + mt * CG) : 0;
     r.kbeg = 0;
     r.kpp = (p.K + BK - 1) / BK;
+    r.lo = r.m0;
+    r.hi = p.M;
   } else {
     const int nm = (p.M + BM * CG - 1) / (BM * CG);
     const int per = nm * nn;
@@ -299,7 +318,7 @@ __device__ __forceinline__ void load_chunk(uint32_t taddr, float (&v)[32]) {
 // common case) is a two-slot insertion.  Same arithmetic as epi_gate below:
 // max, exp(l - max), sequential sum, correctly rounded division, descending
 // selection with ties to the lower expert (matrix.cpp:155-189).
-__device__ __forceinline__ void epi_gate64(const Params& p, uint32_t tbase, int row) {
+__device__ __forceinline__ void epi_gate64(const Params& p, uint32_t tbase, int row, bool valid, uint32_t stage_row) {
   const int E = p.N;
   float ev[64];
   {
@@ -322,14 +341,26 @@ __device__ __forceinline__ void epi_gate64(const Params& p, uint32_t tbase, int 
 #pragma unroll
   for (int i = 0; i < 64; ++i)
     if (i < E) {
-      ev[i] = expf(ev[i] - mx);
+      ev[i] = __expf(ev[i] - mx);  // ex2.approx: a few ulp, inside the bf16 path's 1e-5 score bound
       sum += ev[i];
     }
+  const float rs = __frcp_rn(sum);
 #pragma unroll
-  for (int i = 0; i < 64; ++i) ev[i] = __fdiv_rn(ev[i], sum);
-  const bool valid = row < p.M;
+  for (int i = 0; i < 64; ++i) ev[i] = ev[i] * rs;
   const int k = p.topk;
-  if (valid) {
+  if (valid && stage_row) {
+    // the row through shared memory, then one contiguous bulk store (a warp's
+    // direct float4 stores would each touch 32 rows)
+    bulk_wait_read<0>();  // this lane's previous row has left the staging slot
+#pragma unroll
+    for (int i = 0; i < 64; i += 4)
+      if (i < E)
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(stage_row + i * 4), "f"(ev[i]), "f"(ev[i + 1]),
+                     "f"(ev[i + 2]), "f"(ev[i + 3])
+                     : "memory");
+    fence_proxy_async_smem();
+    bulk_store_1d(p.scores + (int64_t)row * E, stage_row, (uint32_t)E * 4);
+  } else if (valid) {
     float* srow = p.scores + (int64_t)row * E;
     if (E == 64) {
 #pragma unroll
@@ -408,7 +439,7 @@ __device__ __forceinline__ void epi_gate64(const Params& p, uint32_t tbase, int 
 // softmax_rows (matrix.cpp:155-170): max, exp(l - max), sequential sum, divide;
 // topk_rows (matrix.cpp:172-189): descending, ties keep the lower expert.
 template <int BN>
-__device__ __forceinline__ void epi_gate(const Params& p, uint32_t tbase, int row) {
+__device__ __forceinline__ void epi_gate(const Params& p, uint32_t tbase, int row, bool valid) {
   constexpr int KMAX = 8;
   const int E = p.N;
   float mx = -INFINITY;
@@ -436,7 +467,6 @@ __device__ __forceinline__ void epi_gate(const Params& p, uint32_t tbase, int ro
     tv[j] = -INFINITY;
     ti[j] = -1;
   }
-  const bool valid = row < p.M;
   const int k = p.topk;
   for (int c = 0; c < BN / 32; ++c) {
     if (c * 32 >= E) break;
@@ -827,10 +857,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_wait(smem_u32(tfull + acc), acc_phase);
           tc_fence_after();
           const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+          const bool valid = row >= tl.lo && row < tl.hi;
           if constexpr (BN == 64)
-            epi_gate64(p, tb, row);
+            epi_gate64(p, tb, row, valid,
+                       C::GATE_STAGE ? smem_u32(sOut) + (uint32_t)((ew * 32 + lane) * C::GATE_ROW_BYTES) : 0u);
           else
-            epi_gate<BN>(p, tb, row);
+            epi_gate<BN>(p, tb, row, valid);
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(tempty + acc));
@@ -1058,6 +1090,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if constexpr (C::TMA_STORE) {
       if (lane == 0) bulk_wait_all();  // outputs written before the CTA retires
     }
+    if constexpr (C::GATE_STAGE) bulk_wait_all();  // every lane's row stores
   }
   tc_fence_before();
   if (CG == 2)
@@ -1152,6 +1185,11 @@ static void launch_t(Ctx* ctx, const CUtensorMap& ta, const CUtensorMap& tb, con
   int64_t grid = (p.grid_limit > 0 ? std::min<int64_t>(p.grid_limit, ctx->num_sms) : ctx->num_sms) / CG * CG;
   if (max_tiles * CG < grid) grid = max_tiles * CG;
   if (grid < CG) return;
+  if (q.row_split) {
+    if (CG != 1 || p.mode != RAGGED_M || p.tile_group || p.N > BN) shape_error("tc gemm: row_split needs one N tile");
+    q.row_split = (int)grid;
+    q.row_chunks = (int)((ceil_div((int64_t)p.M, grid) + BM - 1) / BM);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(NUM_THREADS);

@@ -122,6 +122,14 @@ struct Params {
   const int* mtile_order;
   // persistent grid cap (0: all SMs); SMs left free run the concurrent push
   int grid_limit;
+  // RAGGED_M without tile_group and N <= BN (the gate): nonzero asks launch()
+  // for balanced contiguous row ranges, one per persistent CTA -- slot s owns
+  // rows [s*M/S, (s+1)*M/S) and walks them in 128-row chunks, the last chunk
+  // shifted back to end at the range end (its overlap recomputed, stored
+  // once) -- instead of whole 128-row tiles dealt round-robin, whose
+  // ceil(M/128/S) vs floor(...) split leaves SMs idle for a whole tile.
+  // launch() replaces it with S and sets row_chunks.
+  int row_split, row_chunks;
   // optional clock probe (Ctx::d_probe slot): CTA 0 writes (clock64,
   // globaltimer) at its start and end
   unsigned long long* probe;

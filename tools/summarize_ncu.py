@@ -23,8 +23,7 @@ PROF = os.path.join(ROOT, "profiles")
 # issue order of one bf16 single-GPU step (layer.cu): data gradients first
 STEP_ORDER = ["gate", "plan_hist", "plan_colscan", "plan_offsets", "plan_rank", "scatter", "fc1", "fc2", "gather_combine",
               "gcb", "dgrad_fc2", "dgrad_fc1", "gate_dx", "scatter_bwd", "wgrad_order", "wgrad_fc2", "db2_colsum",
-              "db2_reduce",
-              "wgrad_fc1", "db1_reduce", "gate_dwg", "gate_dwg_reduce"]
+              "db1_db2_reduce", "wgrad_fc1", "gate_dwg", "gate_dwg_reduce"]
 
 
 def short(name):
