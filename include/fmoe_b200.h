@@ -63,6 +63,11 @@ int64_t fmoe_ctx_launches(const fmoe_ctx* ctx);
  * 16 gate d_x + scatter_backward. */
 int fmoe_ctx_profile(fmoe_ctx* ctx, int n_steps);
 int fmoe_ctx_profile_read(fmoe_ctx* ctx, float* stage_ms, int n_stages, int* steps_done);
+/* Per profiled step s < n: milliseconds from its first mark to the next
+ * step's first mark (the last step: to its own last mark); 0 for steps not
+ * recorded.  Marks are graph-capturable (event-record nodes), so steps
+ * replayed from a captured CUDA graph are timed too. */
+int fmoe_ctx_profile_step_ms(fmoe_ctx* ctx, float* step_ms, int n);
 /* Effective SM clock of the expert GEMMs: arm max_launches probe slots
  * (0 disarms); every expert-GEMM launch then records clock64 / globaltimer at
  * the start and end of its first CTA.  probe_read synchronises and returns the

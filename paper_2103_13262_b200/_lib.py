@@ -71,7 +71,8 @@ class LayerConfig(C.Structure):
 
 EXPORTS = [
     "fmoe_last_error", "fmoe_version", "fmoe_ctx_create", "fmoe_ctx_destroy", "fmoe_ctx_set_stream",
-    "fmoe_ctx_launches", "fmoe_ctx_check", "fmoe_ctx_profile", "fmoe_ctx_profile_read", "fmoe_ctx_clock_probe",
+    "fmoe_ctx_launches", "fmoe_ctx_check", "fmoe_ctx_profile", "fmoe_ctx_profile_read", "fmoe_ctx_profile_step_ms",
+    "fmoe_ctx_clock_probe",
     "fmoe_ctx_clock_probe_read", "fmoe_gate_fwd", "fmoe_gate_bwd", "fmoe_plan_sizes",
     "fmoe_plan_build", "fmoe_scatter", "fmoe_gather_combine", "fmoe_scatter_bwd",
     "fmoe_gather_combine_bwd", "fmoe_experts_fwd", "fmoe_experts_bwd", "fmoe_layer_create",
@@ -116,6 +117,7 @@ def _load():
         "fmoe_ctx_check": [vp],
         "fmoe_ctx_profile": [vp, C.c_int],
         "fmoe_ctx_profile_read": [vp, C.POINTER(C.c_float), C.c_int, C.POINTER(C.c_int)],
+        "fmoe_ctx_profile_step_ms": [vp, C.POINTER(C.c_float), C.c_int],
         "fmoe_ctx_clock_probe": [vp, C.c_int],
         "fmoe_ctx_clock_probe_read": [vp, C.POINTER(C.c_double), C.POINTER(C.c_int)],
         "fmoe_gate_fwd": [vp, C.c_int, vp, vp, i64, i64, i64, i64, vp, vp, vp],

@@ -144,6 +144,24 @@ int fmoe_ctx_profile_read(fmoe_ctx* ctx, float* stage_ms, int n_stages, int* ste
   })
 }
 
+int fmoe_ctx_profile_step_ms(fmoe_ctx* ctx, float* step_ms, int n) {
+  FMOE_GUARD({
+    Ctx* c = C(ctx);
+    Prof* p = c->prof;
+    if (!p) shape_error("profiling not armed");
+    CK(cudaStreamSynchronize(c->stream));
+    for (int s = 0; s < n; ++s) {
+      step_ms[s] = 0.f;
+      if (s >= p->used || p->last[s] < 0) continue;
+      const size_t b = (size_t)s * N_MARKS;
+      // slot s's first mark to the next slot's first mark (the last slot: to its last mark)
+      cudaEvent_t to = (s + 1 < p->used && p->last[s + 1] >= 0) ? p->ev[b + N_MARKS + MARK_FWD_BEGIN]
+                                                              : p->ev[b + p->last[s]];
+      CK(cudaEventElapsedTime(&step_ms[s], p->ev[b + MARK_FWD_BEGIN], to));
+    }
+  })
+}
+
 int fmoe_ctx_clock_probe(fmoe_ctx* ctx, int max_launches) {
   FMOE_GUARD({
     Ctx* c = C(ctx);

@@ -91,7 +91,12 @@ inline void ctx_mark(Ctx* c, int id) {
   Prof* p = c->prof;
   if (!p || c->prof_slot < 0 || c->prof_slot >= p->used) return;
   const size_t base = (size_t)c->prof_slot * N_MARKS;
-  cudaEventRecord(p->ev[base + id], c->stream);
+  // under stream capture the mark becomes an event-record node of the graph
+  // (External), so replayed steps are timed like eager ones
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(c->stream, &cs);
+  cudaEventRecordWithFlags(p->ev[base + id], c->stream,
+                           cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault);
   p->prev[base + id] = p->last[c->prof_slot];
   p->last[c->prof_slot] = (int8_t)id;
 }
