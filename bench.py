@@ -266,7 +266,9 @@ def reference_api_line(cfg: dict, reps: int = 5):
 
 
 def cpu_tokens_for(cores: int) -> int:
-    return max(256, min(4096, 64 * cores))
+    # ~6 s of reference work per rep on 16 host cores at cfg2 (4096 tokens: 64
+    # rows per expert, so its per-expert GEMMs are not starved for rows)
+    return max(256, min(8192, 256 * cores))
 
 
 # --------------------------------------------------------------------- main
