@@ -117,7 +117,16 @@ Layer::Layer(Ctx* c, const fmoe_layer_config& cf) : ctx(c), cfg(cf) {
   if (!ep_mode) tpart = dalloc<float>(owned, experts_bwd_part_floats(plan, d, h));
   if (!ep_mode && bf) relu_bits = dalloc<uint32_t>(owned, cap * (h / 32));
   if (f32tc) f32_planes = dalloc<__nv_bfloat16>(owned, f32_planes_elems(n, d, h, E, el, cap));
+  gather_xs = bf && !ep_mode && n > 0 && gather_enabled();
   if (cfg.world_size > 1) ep_alloc();
+}
+
+// The expanded input rows as a buffer (the operator-level cache view,
+// fmoe_layer_activations): a gathering layer scatters them only when asked.
+void Layer::ensure_xs() {
+  if (xs_fresh || !fwd_done || cfg.world_size > 1) return;
+  scatter(ctx, t, x_saved, cfg.d_m, plan, xs);
+  xs_fresh = true;
 }
 
 Layer::~Layer() {
@@ -234,11 +243,15 @@ void Layer::dispatch_and_experts(const void* x, void* y) {
   }
   plan_build(ctx, idx, plan);                                     // dispatch.cpp:10-47
   ctx_mark(ctx, MARK_PLAN);
-  scatter(ctx, t, x, d, plan, xs);                                // dispatch.cpp:49-59
+  // dispatch.cpp:49-59: a scatter pass, or (bf16, one GPU) folded into fc1's
+  // A-load as a TMA gather of x's rows -- no xs write / re-read
+  const RowGather gth{x, cfg.n_b, plan.src_row};
+  if (!gather_xs) scatter(ctx, t, x, d, plan, xs);
+  xs_fresh = !gather_xs;
   ctx_mark(ctx, MARK_SCATTER);
   const F32Planes pv = planes_view();
   experts_fwd(ctx, t, plan, d, h, params(), xs, hidden, ys, relu_bits, preact_kept ? preact : nullptr, nullptr,
-              nullptr, f32_planes ? &pv : nullptr);  // expert.cpp:85-102
+              nullptr, f32_planes ? &pv : nullptr, gather_xs ? &gth : nullptr);  // expert.cpp:85-102
   gather_combine(ctx, t, ys, d, plan, vals, y);                   // dispatch.cpp:61-78
   ctx_mark(ctx, MARK_GATHER);
   fwd_done = true;
@@ -269,9 +282,11 @@ void Layer::backward(const void* dy, void* dx, cudaEvent_t dx_ready) {
     scatter_bwd(ctx, t, d_xs, d, plan, dx, nullptr);
     ctx_mark(ctx, MARK_GATE_DX);
     if (dx_ready) CK(cudaEventRecord(dx_ready, ctx->stream));
-    if (bf)
+    if (bf) {
+      const RowGather gth{x_saved, cfg.n_b, plan.src_row};
       experts_bwd(ctx, t, plan, d, h, params(), xs, hidden, d_ys, d_xs, grads(), d_pre, tpart, relu_bits,
-                  nullptr, EXPERTS_BWD_WGRAD);
+                  nullptr, EXPERTS_BWD_WGRAD, nullptr, nullptr, nullptr, gather_xs ? &gth : nullptr);
+    }
   } else if (bf) {
     // Data gradients first (expert.cpp:47-48,55), then the gate d_x on the
     // tensor cores (gate.cpp:63, TMA-store epilogue) and scatter_backward
@@ -284,8 +299,9 @@ void Layer::backward(const void* dy, void* dx, cudaEvent_t dx_ready) {
     scatter_bwd(ctx, t, d_xs, d, plan, dx, gdx);
     ctx_mark(ctx, MARK_GATE_DX);
     if (dx_ready) CK(cudaEventRecord(dx_ready, ctx->stream));
+    const RowGather gth{x_saved, cfg.n_b, plan.src_row};
     experts_bwd(ctx, t, plan, d, h, params(), xs, hidden, d_ys, d_xs, grads(), d_pre, tpart, relu_bits,
-                nullptr, EXPERTS_BWD_WGRAD);
+                nullptr, EXPERTS_BWD_WGRAD, nullptr, nullptr, nullptr, gather_xs ? &gth : nullptr);
     gate_dwg_bf16(ctx, x_saved, dz_bf16, n, d, E, part, (float*)dwg);  // gate.cpp:62
     ctx_mark(ctx, MARK_GATE_DWG);
   } else {

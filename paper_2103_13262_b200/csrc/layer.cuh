@@ -24,6 +24,11 @@ struct Layer {
   int32_t* idx = nullptr;
   fmoe_plan plan{};
   void *xs = nullptr, *hidden = nullptr, *ys = nullptr;
+  // bf16, one GPU, FMOE_TC_GATHER=1: fc1 and its weight gradient gather their
+  // input rows from x (TMA gather4, ops.cuh RowGather); xs is then filled only
+  // on request (activations(): the operator-level cache view)
+  bool gather_xs = false, xs_fresh = false;
+  void ensure_xs();
   void* preact = nullptr;  // x*w1 + b1, when kept (fmoe_layer_keep_preact; SIMT / F32 dtypes)
   bool preact_kept = false;
   bool fwd_done = false;

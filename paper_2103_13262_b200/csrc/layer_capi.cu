@@ -48,7 +48,10 @@ int fmoe_layer_activations(fmoe_layer* layer, const void** xs, const void** hidd
                            const void** ys) {
   FMOE_GUARD({
     Layer* l = L(layer);
-    if (xs) *xs = l->xs;
+    if (xs) {
+      l->ensure_xs();
+      *xs = l->xs;
+    }
     if (hidden) *hidden = l->hidden;
     if (preact) *preact = l->preact;
     if (ys) *ys = l->ys;

@@ -207,10 +207,21 @@ static void set_route(tc::Params& p, const RowRoute* r) {
   p.route_world = r->world;
 }
 
+// Off by default: measured ~3x slower than scatter + tile loads on the
+// tensor-bound fc1 / fc1 weight gradient (32 four-row gathers per 16 KiB stage
+// cannot feed the MMA; profiles/r02q_gather_ab.log).  FMOE_TC_GATHER=1 enables.
+bool gather_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("FMOE_TC_GATHER");
+    return v && std::atoi(v) != 0;
+  }();
+  return on;
+}
+
 void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
                  const fmoe_expert_params& w, const void* xs, void* hidden, void* ys,
                  uint32_t* relu_bits, void* preact, const RowRoute* ys_route, const Arrival* arrive,
-                 const F32Planes* planes) {
+                 const F32Planes* planes, const RowGather* gather) {
   const int64_t E = b.n_experts;
   if (E == 0 || b.capacity == 0) return;
   if (t == FMOE_F32 && !ys_route && f32_tc_route(b, d, h)) {  // tensor cores, bf16x3 (f32x.cu)
@@ -250,10 +261,15 @@ void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
   const int cg = pair_mode(b);  // 256-aligned blocks -> CTA-pair tiles
   const int64_t cap = b.capacity;
   const int64_t max_tiles = cap / (128 * cg);
-  {  // fc1: A = xs [cap, d] K-major; B = W1 [E*d, h] MN-major
-    const CUtensorMap ta = tc::make_tmap(xs, d, cap, d * 2, 64, 128);
+  {  // fc1: A = xs [cap, d] K-major (or its rows gathered from x); B = W1 [E*d, h] MN-major
+    const CUtensorMap ta = gather ? tc::make_tmap(gather->x, d, gather->n_b, d * 2, 64, 1)
+                                  : tc::make_tmap(xs, d, cap, d * 2, 64, 128);
     const CUtensorMap tb = tc::make_tmap(w.w1, h, E * d, h * 2, 64, 64);
     tc::Params p{};
+    if (gather) {
+      p.gather_rows = gather->rows;
+      p.gather_oob = (int)gather->n_b;
+    }
     p.mode = tc::RAGGED_M; p.M = (int)cap; p.N = (int)h; p.K = (int)d;
     p.tile_group = b.tile_expert; p.n_mtiles = b.n_tiles; p.b_group_rows = (int)d;
     p.epi = tc::EPI_BF16; p.C = hidden; p.ldc = h;
@@ -283,7 +299,7 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
                  const fmoe_expert_params& w, const void* xs, const void* hidden, const void* d_ys,
                  void* d_xs, const fmoe_expert_grads& g, void* d_pre, float* part_ws,
                  const uint32_t* relu_bits, const void* mask, int phase, const RowRoute* dxs_route,
-                 const Arrival* arrive, const F32Planes* planes) {
+                 const Arrival* arrive, const F32Planes* planes, const RowGather* gather) {
   const int64_t E = b.n_experts;
   if (E == 0) return;
   if (t == FMOE_F32 && phase == EXPERTS_BWD_ALL && !dxs_route && part_ws && f32_tc_route(b, d, h)) {
@@ -399,10 +415,15 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
     tc::launch(ctx, 256, false, false, ta, tb, p, max_tiles * ceil_div(d, 256), cg);
     ctx_mark(ctx, MARK_DGRAD1);
   }
-  if (do_wgrad) {  // wgrad fc1: d_w1[e] = xs_e^T d_pre_e  (M = d, N = h)
-    const CUtensorMap ta = tc::make_tmap(xs, d, cap, d * 2, 64, 64);
+  if (do_wgrad) {  // wgrad fc1: d_w1[e] = xs_e^T d_pre_e  (M = d, N = h; xs rows gathered from x when asked)
+    const CUtensorMap ta = gather ? tc::make_tmap(gather->x, d, gather->n_b, d * 2, 64, 1)
+                                  : tc::make_tmap(xs, d, cap, d * 2, 64, 64);
     const CUtensorMap tb = tc::make_tmap(d_pre, h, cap, h * 2, 64, 64);
     tc::Params p{};
+    if (gather) {
+      p.gather_rows = gather->rows;
+      p.gather_oob = (int)gather->n_b;
+    }
     p.mode = tc::RAGGED_K; p.M = (int)d; p.N = (int)h; p.n_groups = (int)E; p.k_offsets = b.offsets;
     p.group_order = group_order;
     p.epi = tc::EPI_F32; p.C = g.d_w1; p.ldc = h; p.c_group_stride = d * h;

@@ -57,10 +57,19 @@ struct F32Planes {
   __nv_bfloat16 *x = nullptr, *wg = nullptr, *dz = nullptr;
   __nv_bfloat16 *xs = nullptr, *hidden = nullptr, *d_ys = nullptr, *d_pre = nullptr, *w1 = nullptr, *w2 = nullptr;
 };
+// bf16, one GPU: the expanded input rows xs[r] = x[plan.src_row[r]] read straight
+// from x by TMA gather4 in fc1 and in the fc1 weight gradient instead of from a
+// scattered copy (tc::Params::gather_rows); `xs` is then not read.
+struct RowGather {
+  const void* x = nullptr;       // [n_b, d] bf16
+  int64_t n_b = 0;
+  const int32_t* rows = nullptr;  // plan.src_row: [capacity], -1 = padding
+};
 void experts_fwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t h,
                  const fmoe_expert_params& w, const void* xs, void* hidden, void* ys,
                  uint32_t* relu_bits = nullptr, void* preact = nullptr, const RowRoute* ys_route = nullptr,
-                 const Arrival* arrive = nullptr, const F32Planes* planes = nullptr);
+                 const Arrival* arrive = nullptr, const F32Planes* planes = nullptr,
+                 const RowGather* gather = nullptr);
 // preact (SIMT dtypes only, optional): also keep x*w1 + b1 before the relu
 // (ForwardCache::preact, expert.hpp:31-35).
 // d_pre_ws: [capacity, h] dtype scratch; mask (SIMT dtypes only, optional): the
@@ -83,7 +92,10 @@ void experts_bwd(Ctx* ctx, fmoe_dtype t, const fmoe_plan& b, int64_t d, int64_t 
                  void* d_xs, const fmoe_expert_grads& g, void* d_pre_ws, float* part_ws,
                  const uint32_t* relu_bits = nullptr, const void* mask = nullptr,
                  int phase = EXPERTS_BWD_ALL, const RowRoute* dxs_route = nullptr,
-                 const Arrival* arrive = nullptr, const F32Planes* planes = nullptr);
+                 const Arrival* arrive = nullptr, const F32Planes* planes = nullptr,
+                 const RowGather* gather = nullptr);
+// FMOE_TC_GATHER=1 enables the gathered A-loads (off by default: slower, see ops.cu)
+bool gather_enabled();
 // true when an FMOE_F32 expert call takes the tensor-core route: a 128-row
 // aligned plan with its tile table, d_m and d_h multiples of 64, and
 // FMOE_F32_SIMT unset (=1 keeps the SIMT fp32 kernels, the reference's order)

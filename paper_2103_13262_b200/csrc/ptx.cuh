@@ -230,6 +230,25 @@ __device__ __forceinline__ void tma_load_2d_warp(uint32_t dst, const CUtensorMap
         "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1)
         : "memory");
 }
+// TMA tile::gather4, issued by the calling lane: rows r.x..r.w (row
+// coordinates; past the end = zeros) of a {box_inner x 1} tensor map, box_inner
+// elements from column c0, land as four consecutive 128-byte rows at dst (the
+// tile-load SWIZZLE_128B layout).  CG=2: completion on the LEADER's mbarrier.
+template <int CG>
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int4 r) {
+  if constexpr (CG == 2)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w)
+        : "memory");
+}
 // One k-block (4 x K=16) and its commit under a single elect: descriptors
 // a_lo + i*KA / b_lo + i*KB, high words constant.
 template <int CG, uint32_t KA, uint32_t KB>

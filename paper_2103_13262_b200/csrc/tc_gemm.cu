@@ -700,6 +700,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const Tile tl = decode<BN, CG, C::F32OUT>(p, t);
         const int brow = (p.mode == RAGGED_M) ? tl.g * p.b_group_rows : tl.kbeg;
         if (p.arrive_flags && tl.nkb > 0) wait_rows_arrived(p, tl.g, tl.m0 + row_off, lane);
+        // gathered K-major A: this lane's 4 source rows of the tile, for all its k-blocks
+        int4 grow = make_int4(0, 0, 0, 0);
+        if (!A_MN && p.gather_rows && tl.nkb > 0)
+          grow = __ldg(reinterpret_cast<const int4*>(p.gather_rows + tl.m0 + row_off) + lane);
         // split (bf16x6) passes: kb restarts at 0 for every pass, whose A / B
         // planes come from sel_a / sel_b
         int ph = 0;
@@ -731,7 +735,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             else
               tma_load_2d(dst, m, fb, c0, c1);
           };
-          if (!A_MN) {
+          if (p.gather_rows) {
+            // TMA gather4: K-major A (RAGGED_M) -- lane l brings tile rows 4l..4l+3
+            // of this k-block; MN-major A (RAGGED_K) -- lane l brings K-rows
+            // 4(l%16).. of the k-block into M box l/16
+            int4 r;
+            if (!A_MN) {
+              r = grow;
+            } else {
+              r = __ldg(reinterpret_cast<const int4*>(p.gather_rows + tl.kbeg + kb * BK) + (lane & 15));
+            }
+            r.x = r.x < 0 ? p.gather_oob : r.x;
+            r.y = r.y < 0 ? p.gather_oob : r.y;
+            r.z = r.z < 0 ? p.gather_oob : r.z;
+            r.w = r.w < 0 ? p.gather_oob : r.w;
+            if (!A_MN)
+              tma_gather4<CG>(a_dst + lane * 512, mA, fb, kb * BK, r);
+            else
+              tma_gather4<CG>(a_dst + (lane >> 4) * 8192 + (lane & 15) * 512, mA, fb,
+                              tl.m0 + row_off + 64 * (lane >> 4), r);
+          } else if (!A_MN) {
             load(a_dst, mA, kb * BK, tl.m0 + row_off);
           } else {
 #pragma unroll

@@ -122,6 +122,14 @@ struct Params {
   const int* mtile_order;
   // persistent grid cap (0: all SMs); SMs left free run the concurrent push
   int grid_limit;
+  // A operand gathered by TMA tile::gather4 (the single-GPU bf16 layer: no
+  // scatter pass): row r of the expanded layout is row
+  // gather_rows[r] of the A tensor map's matrix (x, box {64, 1}); -1 = padding
+  // (read as zeros).  RAGGED_M with a K-major A (fc1): each producer lane
+  // gathers 4 of the tile's rows per k-block; RAGGED_K with an MN-major A (the
+  // fc1 weight gradient, A = x^T): the k-block's 64 K-rows, 4 per lane.
+  const int* gather_rows;
+  int gather_oob;  // a row coordinate past the end of x
   // RAGGED_M without tile_group and N <= BN (the gate): nonzero asks launch()
   // for balanced contiguous row ranges, one per persistent CTA -- slot s owns
   // rows [s*M/S, (s+1)*M/S) and walks them in 128-row chunks, the last chunk
