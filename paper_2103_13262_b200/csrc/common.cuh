@@ -6,6 +6,8 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cstdlib>
+#include <utility>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -105,6 +107,37 @@ inline int ctx_take_slot(Ctx* c) {
   Prof* p = c->prof;
   c->prof_slot = (p && p->used < p->steps) ? p->used++ : -1;
   return c->prof_slot;
+}
+
+// ------------------------------------------- programmatic dependent launch
+// Back-to-back kernels of one stage with no profiling mark between them (the
+// plan's scan / offsets / rank, scatter_backward after the gate d_x GEMM, the
+// split reduces) are launched with programmatic stream serialization: the
+// next grid is scheduled while the previous one drains, and executes
+// pdl_wait() (griddepcontrol.wait) before touching memory, so only launch
+// latency and block setup overlap -- never data.  FMOE_PDL=0 launches plainly.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("FMOE_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 // ------------------------------------------------------------- type traits

@@ -102,6 +102,7 @@ __global__ void dlogits_kernel(const A* __restrict__ scores, const int32_t* __re
 
 __global__ void reduce_splits_kernel(const float* __restrict__ part, int64_t n_splits, int64_t n,
                                      float* __restrict__ out) {
+  pdl_wait();  // launched right behind the split-K GEMM
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   float acc = 0.f;
@@ -139,7 +140,8 @@ void gate_dlogits(Ctx* ctx, fmoe_dtype t, const void* scores, const int32_t* idx
 
 void reduce_splits(Ctx* ctx, const float* part, int64_t n_splits, int64_t n, float* out) {
   if (n == 0) return;
-  reduce_splits_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, ctx->stream>>>(part, n_splits, n, out);
+  CK(launch_pdl(reduce_splits_kernel, dim3((unsigned)ceil_div(n, 256)), dim3(256), 0, ctx->stream, part, n_splits, n,
+                out));
   CK_LAUNCH(ctx);
 }
 

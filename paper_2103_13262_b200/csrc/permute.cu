@@ -163,6 +163,7 @@ __global__ void gather_combine_kernel(const T* __restrict__ ys, int64_t d, fmoe_
 template <typename T, int KM = 4>
 __global__ void scatter_bwd_kernel(const T* __restrict__ d_xs, int64_t d, fmoe_plan p,
                                    const T* __restrict__ addend, T* __restrict__ dx) {
+  pdl_wait();  // launched right behind the gate d_x GEMM (scatter_bwd below)
   using A = AccOf<T>;
   constexpr int V = Vec<T>::N;
   const int64_t i = warp_id_global();
@@ -527,6 +528,7 @@ __global__ void __launch_bounds__(256) tile_colsum_kernel(const __nv_bfloat16* _
 __global__ void reduce_tile_partials_kernel(const float* __restrict__ part1, int64_t n1, float* __restrict__ out1,
                                             const float* __restrict__ part2, int64_t n2, float* __restrict__ out2,
                                             const int32_t* __restrict__ offsets) {
+  pdl_wait();
   const int e = blockIdx.y;
   const int64_t nb1 = (n1 + blockDim.x - 1) / blockDim.x;
   const bool first = blockIdx.x < nb1;
@@ -585,7 +587,8 @@ void reduce_tile_partials(Ctx* ctx, const float* part, int64_t n_cols, const int
   if (n_blocks == 0 || (n_cols == 0 && n_cols2 == 0)) return;
   if (!part2) n_cols2 = 0;
   dim3 grid((unsigned)(ceil_div(n_cols, 256) + ceil_div(n_cols2, 256)), (unsigned)n_blocks);
-  reduce_tile_partials_kernel<<<grid, 256, 0, ctx->stream>>>(part, n_cols, out, part2, n_cols2, out2, offsets);
+  CK(launch_pdl(reduce_tile_partials_kernel, grid, dim3(256), 0, ctx->stream, part, n_cols, out,
+                (const float*)part2, n_cols2, out2, offsets));
   CK_LAUNCH(ctx);
 }
 
@@ -621,13 +624,11 @@ void scatter_bwd(Ctx* ctx, fmoe_dtype t, const void* d_xs, int64_t d, const fmoe
   dispatch_dtype(t, [&](auto* tag) {
     using T = std::remove_pointer_t<decltype(tag)>;
     if (p.k <= 2)
-      scatter_bwd_kernel<T, 2><<<grid, 256, 0, ctx->stream>>>(reinterpret_cast<const T*>(d_xs), d, p,
-                                                             reinterpret_cast<const T*>(addend),
-                                                             reinterpret_cast<T*>(dx));
+      CK(launch_pdl(scatter_bwd_kernel<T, 2>, dim3(grid), dim3(256), 0, ctx->stream, reinterpret_cast<const T*>(d_xs),
+                    d, p, reinterpret_cast<const T*>(addend), reinterpret_cast<T*>(dx)));
     else
-      scatter_bwd_kernel<T, 4><<<grid, 256, 0, ctx->stream>>>(reinterpret_cast<const T*>(d_xs), d, p,
-                                                             reinterpret_cast<const T*>(addend),
-                                                             reinterpret_cast<T*>(dx));
+      CK(launch_pdl(scatter_bwd_kernel<T, 4>, dim3(grid), dim3(256), 0, ctx->stream, reinterpret_cast<const T*>(d_xs),
+                    d, p, reinterpret_cast<const T*>(addend), reinterpret_cast<T*>(dx)));
   });
   CK_LAUNCH(ctx);
 }

@@ -74,6 +74,7 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
 // place, each chunk's exclusive prefix inside its expert column (chunk order).
 __global__ void plan_colscan(int32_t* __restrict__ chunk_hist, int n_chunks, int n_experts,
                              int32_t* __restrict__ counts) {
+  pdl_wait();
   const int e = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (e >= n_experts) return;
@@ -105,6 +106,7 @@ __global__ void plan_colscan(int32_t* __restrict__ chunk_hist, int n_chunks, int
 __global__ void plan_offsets(const int32_t* __restrict__ counts, int n_experts, int align,
                              int32_t* __restrict__ offsets, int32_t* __restrict__ src_row,
                              int32_t* __restrict__ tile_expert, int32_t* __restrict__ n_tiles) {
+  pdl_wait();
   extern __shared__ int32_t sh[];  // [n_experts] aligned counts -> exclusive offsets
   int32_t* acnt = sh;
   __shared__ int32_t warp_tot[32];
@@ -152,6 +154,7 @@ __global__ void plan_rank(const int32_t* __restrict__ idx, int64_t nk, int k, in
                           const int32_t* __restrict__ chunk_base, const int32_t* __restrict__ offsets,
                           int32_t* __restrict__ src_row,
                           int32_t* __restrict__ slot, int32_t* __restrict__ inverse_pos) {
+  pdl_wait();
   extern __shared__ int32_t sh[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int32_t* run = sh + w * n_experts;
@@ -231,18 +234,19 @@ void plan_build(Ctx* ctx, const int32_t* topk_idx, const fmoe_plan& p) {
     CK_LAUNCH(ctx);
   }
   if (nk > 0) {
-    plan_colscan<<<(unsigned)ceil_div((int64_t)E * 32, 256), 256, 0, ctx->stream>>>(chunk_hist, (int)chunks, E,
-                                                                                    p.counts);
+    CK(launch_pdl(plan_colscan, dim3((unsigned)ceil_div((int64_t)E * 32, 256)), dim3(256), 0, ctx->stream, chunk_hist,
+                  (int)chunks, E, p.counts));
     CK_LAUNCH(ctx);
   } else {
     CK(cudaMemsetAsync(p.counts, 0, (size_t)E * 4, ctx->stream));
   }
-  plan_offsets<<<1, 1024, (size_t)E * 4, ctx->stream>>>(p.counts, E, (int)p.align, p.offsets, p.src_row,
-                                                        p.align % 128 == 0 ? p.tile_expert : nullptr, p.n_tiles);
+  CK(launch_pdl(plan_offsets, dim3(1), dim3(1024), (size_t)E * 4, ctx->stream, p.counts, E, (int)p.align, p.offsets,
+                p.src_row, p.align % 128 == 0 ? p.tile_expert : (int32_t*)nullptr, p.n_tiles));
   CK_LAUNCH(ctx);
   if (nk > 0) {
-    plan_rank<<<grid, 32 * kWarpsPerCta, smem, ctx->stream>>>(topk_idx, nk, (int)p.k, E, (int)chunks, chunk_hist,
-                                                              p.offsets, p.src_row, p.slot, p.inverse_pos);
+    CK(launch_pdl(plan_rank, dim3(grid), dim3(32 * kWarpsPerCta), smem, ctx->stream, topk_idx, nk, (int)p.k, E,
+                  (int)chunks, (const int32_t*)chunk_hist, (const int32_t*)p.offsets, p.src_row, p.slot,
+                  p.inverse_pos));
     CK_LAUNCH(ctx);
   }
 }
