@@ -110,12 +110,13 @@ inline int ctx_take_slot(Ctx* c) {
 }
 
 // ------------------------------------------- programmatic dependent launch
-// Back-to-back kernels of one stage with no profiling mark between them (the
-// plan's scan / offsets / rank, scatter_backward after the gate d_x GEMM, the
-// split reduces) are launched with programmatic stream serialization: the
-// next grid is scheduled while the previous one drains, and executes
-// pdl_wait() (griddepcontrol.wait) before touching memory, so only launch
-// latency and block setup overlap -- never data.  FMOE_PDL=0 launches plainly.
+// The single-GPU layer's kernels (plan, permutes, reduces, the tcgen05 GEMMs)
+// are launched with programmatic stream serialization: the next grid is
+// scheduled while the previous one drains and executes pdl_wait()
+// (griddepcontrol.wait) before touching memory, so only launch latency and
+// block setup (for the GEMMs: barriers, TMEM, tensor maps) overlap -- never
+// data.  A profiling mark (event record) between two kernels disables the
+// overlap there.  FMOE_PDL=0 launches plainly.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 inline bool pdl_enabled() {
   static const bool on = [] {

@@ -67,6 +67,7 @@ __device__ __forceinline__ int64_t pad_row(const fmoe_plan& p, int64_t w) {
 // scatter (collectives.cpp:146-203) become one pass.
 __global__ void scatter_kernel(const uint8_t* __restrict__ x, int64_t row_bytes, fmoe_plan p,
                                uint8_t* __restrict__ xs, ScatterRoute route) {
+  pdl_wait();
   const int64_t w = warp_id_global();
   const int lane = threadIdx.x & 31;
   const int k = (int)p.k;
@@ -120,6 +121,7 @@ __global__ void scatter_kernel(const uint8_t* __restrict__ x, int64_t row_bytes,
 template <typename T, typename S>
 __global__ void gather_combine_kernel(const T* __restrict__ ys, int64_t d, fmoe_plan p,
                                       const S* __restrict__ w, T* __restrict__ y) {
+  pdl_wait();
   using A = AccOf<T>;
   constexpr int V = Vec<T>::N;
   const int64_t i = warp_id_global();
@@ -275,6 +277,7 @@ __global__ void __launch_bounds__(256, FMOE_GCB_MINB) gcb_kernel(const T* __rest
                            const S* __restrict__ w, T* __restrict__ d_ys, S* __restrict__ d_w,
                            const float* __restrict__ scores, const int32_t* __restrict__ topk_idx,
                            __nv_bfloat16* __restrict__ dz, ScatterRoute route) {
+  pdl_wait();
   using A = AccOf<T>;
   constexpr int V = Vec<T>::N;
   const int64_t i = warp_id_global();
@@ -494,6 +497,7 @@ __global__ void block_colsum_kernel(const T* __restrict__ src, int64_t n_cols,
 // rows of loads in flight, so the pass streams d_ys at HBM rate.
 __global__ void __launch_bounds__(256) tile_colsum_kernel(const __nv_bfloat16* __restrict__ src, int64_t n_cols,
                                                           const int32_t* __restrict__ n_tiles, float* __restrict__ part) {
+  pdl_wait();
   const int64_t t = blockIdx.x;
   if (t >= __ldg(n_tiles)) return;
   const int64_t nv = n_cols / 8;
@@ -554,6 +558,7 @@ __global__ void reduce_tile_partials_kernel(const float* __restrict__ part1, int
 // order[rank] = group, ranked by decreasing row count (offsets[g+1] -
 // offsets[g]), ties by index: O(G^2) comparisons in one block.
 __global__ void order_groups_kernel(const int32_t* __restrict__ offsets, int G, int32_t* __restrict__ order) {
+  pdl_wait();
   for (int g = threadIdx.x; g < G; g += blockDim.x) {
     const int c = offsets[g + 1] - offsets[g];
     int rank = 0;
@@ -569,7 +574,7 @@ __global__ void order_groups_kernel(const int32_t* __restrict__ offsets, int G, 
 
 void order_groups_desc(Ctx* ctx, const int32_t* offsets, int64_t groups, int32_t* order) {
   if (groups <= 0) return;
-  order_groups_kernel<<<1, 1024, 0, ctx->stream>>>(offsets, (int)groups, order);
+  CK(launch_pdl(order_groups_kernel, dim3(1), dim3(1024), 0, ctx->stream, offsets, (int)groups, order));
   CK_LAUNCH(ctx);
 }
 
@@ -578,7 +583,8 @@ void tile_colsum(Ctx* ctx, const __nv_bfloat16* src, int64_t n_cols, const int32
   if (max_tiles == 0 || n_cols == 0) return;
   if (n_cols % 8) shape_error("tile_colsum: columns must be a multiple of 8");
   const int threads = (int)std::min<int64_t>(256, ceil_div(n_cols / 8, 32) * 32);
-  tile_colsum_kernel<<<(unsigned)max_tiles, threads, 0, ctx->stream>>>(src, n_cols, n_tiles, part);
+  CK(launch_pdl(tile_colsum_kernel, dim3((unsigned)max_tiles), dim3(threads), 0, ctx->stream, src, n_cols, n_tiles,
+                part));
   CK_LAUNCH(ctx);
 }
 
@@ -597,10 +603,8 @@ void scatter(Ctx* ctx, fmoe_dtype t, const void* x, int64_t d, const fmoe_plan& 
   const int64_t warps = p.n_b + (p.align > 1 ? p.n_experts * p.align : 0);
   if (warps == 0) return;
   const unsigned grid = (unsigned)ceil_div(warps * 32, 256);
-  scatter_kernel<<<grid, 256, 0, ctx->stream>>>(reinterpret_cast<const uint8_t*>(x),
-                                                d * (int64_t)dtype_size(t), p,
-                                                reinterpret_cast<uint8_t*>(xs),
-                                                route ? *route : ScatterRoute{});
+  CK(launch_pdl(scatter_kernel, dim3(grid), dim3(256), 0, ctx->stream, reinterpret_cast<const uint8_t*>(x),
+                d * (int64_t)dtype_size(t), p, reinterpret_cast<uint8_t*>(xs), route ? *route : ScatterRoute{}));
   CK_LAUNCH(ctx);
 }
 
@@ -611,8 +615,8 @@ void gather_combine(Ctx* ctx, fmoe_dtype t, const void* ys, int64_t d, const fmo
   dispatch_dtype(t, [&](auto* tag) {
     using T = std::remove_pointer_t<decltype(tag)>;
     using S = typename ScoreOf<T>::type;
-    gather_combine_kernel<T, S><<<grid, 256, 0, ctx->stream>>>(
-        reinterpret_cast<const T*>(ys), d, p, reinterpret_cast<const S*>(w), reinterpret_cast<T*>(y));
+    CK(launch_pdl(gather_combine_kernel<T, S>, dim3(grid), dim3(256), 0, ctx->stream, reinterpret_cast<const T*>(ys),
+                  d, p, reinterpret_cast<const S*>(w), reinterpret_cast<T*>(y)));
   });
   CK_LAUNCH(ctx);
 }
@@ -644,10 +648,10 @@ void gather_combine_bwd(Ctx* ctx, fmoe_dtype t, const void* dy, const void* ys, 
   dispatch_dtype(t, [&](auto* tag) {
     using T = std::remove_pointer_t<decltype(tag)>;
     using S = typename ScoreOf<T>::type;
-    gcb_kernel<T, S><<<grid, 256, 0, ctx->stream>>>(
-        reinterpret_cast<const T*>(dy), reinterpret_cast<const T*>(ys), d, p,
-        reinterpret_cast<const S*>(w), reinterpret_cast<T*>(d_ys), reinterpret_cast<S*>(d_w),
-        reinterpret_cast<const float*>(scores), topk_idx, dz, route ? *route : ScatterRoute{});
+    CK(launch_pdl(gcb_kernel<T, S>, dim3(grid), dim3(256), 0, ctx->stream, reinterpret_cast<const T*>(dy),
+                  reinterpret_cast<const T*>(ys), d, p, reinterpret_cast<const S*>(w), reinterpret_cast<T*>(d_ys),
+                  reinterpret_cast<S*>(d_w), reinterpret_cast<const float*>(scores), topk_idx, dz,
+                  route ? *route : ScatterRoute{}));
   });
   CK_LAUNCH(ctx);
 }

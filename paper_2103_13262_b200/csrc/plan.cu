@@ -30,6 +30,7 @@ constexpr int kWarpsPerCta = 4;
 // expert's column contiguously.
 __global__ void plan_hist(const int32_t* __restrict__ idx, int64_t nk, int n_experts, int n_chunks,
                           int32_t* __restrict__ chunk_hist, int* __restrict__ err) {
+  pdl_wait();
   extern __shared__ int32_t sh[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int32_t* hist = sh + w * n_experts;
@@ -229,8 +230,8 @@ void plan_build(Ctx* ctx, const int32_t* topk_idx, const fmoe_plan& p) {
   });
   const unsigned grid = (unsigned)std::max<int64_t>(1, ceil_div(chunks, kWarpsPerCta));
   if (nk > 0) {
-    plan_hist<<<grid, 32 * kWarpsPerCta, smem, ctx->stream>>>(topk_idx, nk, E, (int)chunks, chunk_hist,
-                                                              ctx->d_error);
+    CK(launch_pdl(plan_hist, dim3(grid), dim3(32 * kWarpsPerCta), smem, ctx->stream, topk_idx, nk, E, (int)chunks,
+                  chunk_hist, ctx->d_error));
     CK_LAUNCH(ctx);
   }
   if (nk > 0) {

@@ -681,6 +681,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   else
     __syncthreads();
   tc_fence_after();
+  // programmatic dependent launch: barrier init, TMEM allocation and the
+  // tensor-map prefetch above overlap the previous kernel's tail; nothing
+  // below touches global memory before it completes
+  pdl_wait();
   const uint32_t tmem_base = *tmem_slot;
   const int total = total_tiles<BN, CG>(p);
   const int row_off = (int)rank * BM;             // this CTA's rows inside a pair tile
@@ -1218,13 +1222,15 @@ static void launch_t(Ctx* ctx, const CUtensorMap& ta, const CUtensorMap& tb, con
   cfg.blockDim = dim3(NUM_THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = ctx->stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   if (q.phases > 1 && (!split || !C::F32OUT)) shape_error("tc gemm: split product without its planes / fp32 output");
   const SplitMaps sm = split ? *split : SplitMaps{ta, ta, tb, tb};
   CK(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc_out, sm, q));

@@ -19,7 +19,9 @@ v, wl, r, f = sys.argv[1:]
 try:
     l = json.loads(open(f).read().strip().splitlines()[-1])
     s = l["stages_ms"]
+    e2e = (l.get("e2e") or {}).get("value")
     print(f"{wl} r{r} {v}: {l['value']/1e6:.3f}M ms={l['ms_per_step']:.3f} gemm_mhz={l['clocks'].get('gemm_sm_mhz_effective')} "
+          + (f"e2e={e2e/1e6:.3f}M " if e2e else "")
           + " ".join(f"{k}={1000*x:.1f}" for k, x in s.items()))
 except Exception as e:
     print(f"{wl} r{r} {v}: failed {e}")
