@@ -59,7 +59,8 @@ int64_t fmoe_ctx_launches(const fmoe_ctx* ctx);
  * milliseconds between the previous mark and this one over the recorded
  * steps.  Stage order: 0 -, 1 gate, 2 plan, 3 scatter, 4 fc1, 5 fc2,
  * 6 gather_combine, 7 (fwd->bwd gap), 8 gather_combine_bwd, 9 dgrad fc2,
- * 10 wgrad fc2, 11 db2, 12 dgrad fc1, 13 wgrad fc1, 14 db1, 15 gate d_wg,
+ * 10 wgrad fc2, 11 db2 (bf16: d_b2 column sums + the d_b1 and d_b2 reduce),
+ * 12 dgrad fc1, 13 wgrad fc1, 14 db1 (0 on the bf16 path), 15 gate d_wg,
  * 16 gate d_x + scatter_backward. */
 int fmoe_ctx_profile(fmoe_ctx* ctx, int n_steps);
 int fmoe_ctx_profile_read(fmoe_ctx* ctx, float* stage_ms, int n_stages, int* steps_done);
